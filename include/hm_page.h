@@ -1,0 +1,233 @@
+/*
+ * hm_page.h — C-ABI of the B200-native page-granular update path
+ * (Angel-PTM, arxiv 2303.02868; reference package `hiermem` 0.1.0).
+ *
+ * The reference is pure Python/numpy and has no FFI of its own: its
+ * boundary is the Python API re-exported by hiermem/__init__.py:8-74.
+ * Every entry point below replaces one reference operation (cited as
+ * hiermem/<file>.py:<line>, i.e. /root/reference/pkg/src/hiermem/...).
+ * The Python host package (paper_2303_02868_b200) binds these with ctypes;
+ * INTEGRATION.md shows the binding a maintainer would add to `hiermem`.
+ *
+ * Conventions
+ *  - extern "C", plain pointers and sizes, no torch/C++ types.
+ *  - Every function returns an int status: HM_OK (0) or one of HM_ERR_*.
+ *    The thread-local message is read with hm_last_error(); allocation
+ *    failures also carry (requested_bytes, available_bytes) through
+ *    hm_last_error_bytes(), mirroring hiermem/errors.py:8-14.
+ *  - Device entry points are asynchronous on the caller's cudaStream_t
+ *    (passed as void*), never allocate or free device memory, and never
+ *    synchronise the device.  No CPU fallback exists.
+ *  - Element offsets are in elements of the named buffer, byte offsets
+ *    in bytes.  Kernels handle any alignment; 16/32-byte aligned runs
+ *    take the 128/256-bit vector path.
+ */
+#ifndef HM_PAGE_H
+#define HM_PAGE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map to hiermem/errors.py:4-39) ---------------------- */
+#define HM_OK              0
+#define HM_ERR_CONFIG      1   /* ConfigError      hiermem/errors.py:4     */
+#define HM_ERR_ALLOCATION  2   /* AllocationError  hiermem/errors.py:8-14  */
+#define HM_ERR_MOVE        3   /* MoveError        hiermem/errors.py:17    */
+#define HM_ERR_PROTOCOL    4   /* ProtocolError    hiermem/errors.py:38    */
+#define HM_ERR_KEY         5   /* KeyError (unknown page / tensor id)      */
+#define HM_ERR_CUDA        6   /* CUDA runtime error (message has details) */
+#define HM_ERR_INVALID     7   /* bad argument to the C-ABI itself         */
+
+/* ---- element types ------------------------------------------------------ */
+#define HM_DT_F16   1   /* IEEE binary16 (the reference's np.float16)        */
+#define HM_DT_BF16  2   /* bfloat16 (north-star parameter/gradient type)     */
+#define HM_DT_F32   3   /* binary32 master/moment type                       */
+
+/* ---- tiers (hiermem/pagemem.py:29-32) and tensor kinds (footprint.py:22) */
+#define HM_TIER_GPU 0
+#define HM_TIER_CPU 1
+#define HM_TIER_SSD 2
+#define HM_KIND_PARAM16 0
+#define HM_KIND_GRAD16  1
+#define HM_KIND_OPTIM32 2
+#define HM_KIND_ACT16   3
+
+const char* hm_last_error(void);
+void        hm_last_error_bytes(int64_t* requested_bytes, int64_t* available_bytes);
+int         hm_abi_version(void);   /* bumped on any layout change below */
+int         hm_device_chunk_elems(void);  /* HM_ADAM_CHUNK, the kernel unit */
+
+/* ======================================================================== *
+ *  Host page table (replaces hiermem/pagemem.py:111-446, metadata only).   *
+ *  One handle = one PageManager (hiermem/pagemem.py:188-229).  Reentrant   *
+ *  per handle, not thread-safe per handle: callers serialise mutations,    *
+ *  exactly the single-owner contract of hiermem/pagemem.py:11-12.          *
+ * ======================================================================== */
+typedef struct hm_pagetable hm_pagetable;
+
+int hm_pt_create(hm_pagetable** out);
+int hm_pt_destroy(hm_pagetable* pt);
+/* TierPool.__init__ + PageManager.__init__ pool loop (pagemem.py:114-134,
+ * 195-203).  first_page_id < 0 means "next free global id" (manager order). */
+int hm_pt_add_pool(hm_pagetable* pt, int tier, int64_t capacity_bytes,
+                   int64_t page_bytes, int64_t first_page_id);
+/* PageManager.allocate (pagemem.py:233-283). */
+int hm_pt_allocate(hm_pagetable* pt, int tier, int kind, int64_t bytes, int64_t* tensor_id);
+/* PageManager.release (pagemem.py:285-299). */
+int hm_pt_release(hm_pagetable* pt, int64_t tensor_id, int64_t* freed_bytes);
+/* PageManager.page_move (pagemem.py:303-334); out = TransferDescriptor
+ * {bytes, src_tier, dst_tier, page_id, new_page_id} (pagemem.py:102-108). */
+int hm_pt_page_move(hm_pagetable* pt, int64_t page_id, int target_tier, int64_t out[5]);
+/* PageManager.tensor_merge (pagemem.py:338-407).  out = {moved_chunks, first_page}. */
+int hm_pt_tensor_merge(hm_pagetable* pt, int64_t tensor_id, int64_t out[2]);
+
+/* Introspection (Page/ManagedTensor/TierPool/state_dict, pagemem.py:46-99,
+ * 136-165, 411-446).  Array outputs return the element count; pass cap=0
+ * to query the size. */
+int     hm_pt_num_pools(const hm_pagetable* pt);
+/* out = {tier, capacity_bytes, page_bytes, first_page_id, num_pages,
+ *        free_pages, allocations, releases, moves_in, moves_out,
+ *        peak_allocated_pages, occupied_bytes_of_allocated_pages} */
+int     hm_pt_pool_info(const hm_pagetable* pt, int pool_index, int64_t out[12]);
+int64_t hm_pt_allocated_pages(const hm_pagetable* pt, int tier, int64_t* out, int64_t cap);
+int64_t hm_pt_free_pages(const hm_pagetable* pt, int tier, int64_t* out, int64_t cap);
+/* out = {tier, total_bytes, n_occupants, then per occupant
+ *        (tensor_id, bytes, shareable, byte_offset)}  (max 2 occupants) */
+int     hm_pt_page_info(const hm_pagetable* pt, int64_t page_id, int64_t out[11]);
+int64_t hm_pt_tensor_ids(const hm_pagetable* pt, int64_t* out, int64_t cap);
+/* out = {kind, bytes, tier_or_-1 (NOT_READY), n_pages} */
+int     hm_pt_tensor_info(const hm_pagetable* pt, int64_t tensor_id, int64_t out[4]);
+int64_t hm_pt_tensor_pages(const hm_pagetable* pt, int64_t tensor_id, int64_t* out, int64_t cap);
+/* The physical placement the reference leaves implicit: one triple
+ * (page_id, byte_offset_in_page, bytes) per page of the tensor, in
+ * tensor order.  Occupant slot 0 sits at offset 0, a second occupant is
+ * end-aligned, so any legal pair never overlaps. */
+int64_t hm_pt_tensor_segments(const hm_pagetable* pt, int64_t tensor_id, int64_t* out3, int64_t cap);
+
+/* ======================================================================== *
+ *  Device kernels (sm_100a).                                               *
+ * ======================================================================== */
+#define HM_ADAM_CHUNK 4096   /* elements per CTA work unit */
+
+/* One unit of the fused page-Adam kernel: a run of <= HM_ADAM_CHUNK
+ * elements of one segment (a tensor's share of one page). */
+typedef struct hm_adam_chunk {
+  uint64_t g_off;   /* element offset into the gradient source               */
+  uint64_t s_off;   /* element offset into p32 / m32 / v32                   */
+  uint64_t p_off;   /* element offset into the 16-bit parameter output       */
+  uint32_t n;       /* element count                                         */
+  uint32_t slot;    /* index into the launch's group table                   */
+} hm_adam_chunk;
+
+/* Per-launch, per-group record built by the host (one per MasterState
+ * layer touched by the launch). */
+typedef struct hm_group_launch {
+  uint64_t g_shift;   /* added to g_off: selects the taken gradient buffer   */
+  uint64_t p_shift;   /* added to p_off: selects the p16 publish buffer      */
+  uint32_t group;     /* index into steps[] / applied[]                      */
+  uint32_t flag;      /* index into nonfinite[] / sumsq[] of the gradient    */
+} hm_group_launch;
+
+/* Written by the prologue for the main kernel (device scratch, one per slot). */
+typedef struct hm_group_rt {
+  float    bc1;       /* f32(1 - beta1**step), host-double exact table       */
+  float    bc2;       /* f32(1 - beta2**step)                                */
+  float    gscale;    /* unscale x clip coefficient (1.0f: exact identity)   */
+  uint32_t apply;     /* 0: layer rejected (hiermem/lockfree.py:133-134)     */
+} hm_group_rt;
+
+/* Scalars of AdamHyper (hiermem/lockfree.py:37-42) rounded to f32 exactly as
+ * numpy's weak-scalar promotion does (lockfree.py:135-141). */
+typedef struct hm_adam_hyper {
+  float lr, beta1, one_minus_beta1, beta2, one_minus_beta2, eps;
+  float inv_scale;    /* loss-scale unscale; 1.0f for reference parity       */
+  float max_norm;     /* global grad-norm clip; <= 0 disables               */
+} hm_adam_hyper;
+
+/* Fused take -> update -> publish over page segments: one HBM pass reading
+ * g (16-bit or f32) + p32/m32/v32 and writing p32/m32/v32 + p16.
+ *   hiermem/lockfree.py:127-142 (apply_update), :155-165 (update_layer with
+ *   step rollback), :168-171 + :243-263 (publish cast), :226-241 (take).
+ * The prologue consumes nonfinite[flag] (computed when the gradient was
+ * produced: hm_accumulate / hm_reduce_stats), advances steps[group] only
+ * for applied groups, writes applied[group], clears the consumed flag and
+ * sumsq when consume_flags != 0, and looks up bc1/bc2 in bc_table
+ * (pairs, index = step; must cover every reachable step).
+ * explicit_step > 0 selects the functional apply_update form: the step is
+ * given, steps[] is neither read nor written, and bc_table[0] holds its
+ * (bc1, bc2).  p16 == NULL skips the publish cast.
+ * On a rejected group nothing is written to p32/m32/v32; if p16 != NULL
+ * the unchanged p32 is still cast (the reference publishes after a reject,
+ * hiermem/lockfree.py:631-638). */
+int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
+                 const hm_group_launch* groups, int32_t n_groups,
+                 hm_group_rt* rt_scratch,
+                 const void* g, int g_dtype,
+                 float* p32, float* m32, float* v32,
+                 void* p16, int p16_dtype,
+                 const hm_adam_hyper* hyper,
+                 const float* bc_table, int64_t bc_len, int64_t explicit_step,
+                 int32_t* steps, uint32_t* applied,
+                 uint32_t* nonfinite, double* sumsq, int consume_flags,
+                 void* stream);
+
+/* Elementwise segment chunk used by accumulate / cast / reduce. */
+typedef struct hm_seg_chunk {
+  uint64_t src_off;   /* element offset into src */
+  uint64_t dst_off;   /* element offset into dst */
+  uint32_t n;         /* element count (<= HM_ADAM_CHUNK) */
+  uint32_t slot;      /* index into nonfinite[] / sumsq[] / sums[] */
+} hm_seg_chunk;
+
+/* ParamBuffer.accumulate (hiermem/lockfree.py:210-224):
+ *   dst = rn_dst(f32(dst) + f32(src))   (mode 1: add)
+ *   dst = rn_dst(0.0f + f32(src))       (mode 0: first message into a taken
+ *                                        buffer; == add onto zeros, bitwise)
+ * and, fused into the same pass, nonfinite[slot] |= any(!isfinite(dst)) and
+ * sumsq[slot] += sum(dst^2) (f64) — the layer's reject flag
+ * (lockfree.py:133) and grad-norm term, so the update never re-reads g. */
+int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
+                  const hm_seg_chunk* chunks, int64_t n_chunks, int mode,
+                  uint32_t* nonfinite, double* sumsq, void* stream);
+
+/* RNE dtype conversion over segments: publish cast (lockfree.py:169), take
+ * widen (lockfree.py:234), pack/unpack of typed tensors. */
+int hm_cast(const void* src, int src_dtype, void* dst, int dst_dtype,
+            const hm_seg_chunk* chunks, int64_t n_chunks, void* stream);
+
+/* Read-only statistics over segments: nonfinite flag, f64 sum and f64 sum of
+ * squares per slot (any output may be NULL).  Used for the functional
+ * apply_update check (lockfree.py:133), the post-reduce-scatter check, and
+ * the optional ConservationLedger sums (lockfree.py:218-237, 275-326). */
+int hm_reduce_stats(const void* src, int src_dtype, const hm_seg_chunk* chunks,
+                    int64_t n_chunks, uint32_t* nonfinite, double* sums,
+                    double* sumsq, void* stream);
+
+/* Byte-copy descriptors: page pack/unpack (tensor <-> page pool), page
+ * relocation (page_move / tensor_merge data motion, pagemem.py:303-407). */
+typedef struct hm_copy_desc {
+  uint64_t src_off;   /* bytes */
+  uint64_t dst_off;   /* bytes */
+  uint64_t bytes;
+} hm_copy_desc;
+
+/* Device-side gather/scatter copy of many runs in one launch (16-byte
+ * vector path when src/dst/len are co-aligned). */
+int hm_copy_runs(const void* src, void* dst, const hm_copy_desc* descs,
+                 int64_t n_descs, void* stream);
+
+/* Pinned-host <-> device page swap (the CPU tier of hiermem/simengine.py:
+ * 250-274 and DelayModel state fetch/store, lockfree.py:96-103): one
+ * cudaMemcpyAsync per run on the caller's copy stream (copy engines, no SMs).
+ * kind: 1 = host->device, 2 = device->host, 3 = device->device. */
+int hm_memcpy_runs(const void* src, void* dst, const hm_copy_desc* descs,
+                   int64_t n_descs, int kind, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HM_PAGE_H */

@@ -1,0 +1,227 @@
+// Fused page-Adam (K2 with the take/publish fusions K4/K5 of SURVEY §2.4).
+//
+// One HBM pass per element: read g (2 B bf16/fp16, or 4 B f32) and p32/m32/v32
+// (12 B), write p32/m32/v32 (12 B) and the 16-bit published copy (2 B) —
+// 28 B/param, the algorithmic minimum for the reference chain
+//   take (hiermem/lockfree.py:226-241) -> update_layer (:155-165) ->
+//   apply_update (:127-142) -> publish cast (:168-171, :243-263).
+// The arithmetic is the reference's numpy chain restated op for op with
+// correctly rounded binary32 operations and no contraction (numpy issues one
+// ufunc per operator, so there is no FMA): bit-identical results.
+//   m  = b1*m + (1-b1)*g                 lockfree.py:135
+//   v  = b2*v + (1-b2)*(g*g)             lockfree.py:136
+//   mh = m / f32(1-b1**step)             lockfree.py:137,139
+//   vh = v / f32(1-b2**step)             lockfree.py:138,140
+//   p  = p - (lr*mh) / (sqrt(vh) + eps)  lockfree.py:141
+// The whole-layer reject of lockfree.py:133-134 (+ step rollback :163-164) is
+// decided once per layer by the prologue from the flag that the gradient's
+// producer (hm_accumulate / hm_reduce_stats) fused into its own pass.
+#include "hm_device.cuh"
+#include "hm_error.h"
+
+namespace hm {
+namespace {
+
+constexpr int kPrologueThreads = 1024;
+
+// Per-layer decision: reject flag, step advance, bias-correction lookup,
+// optional global grad-norm clip.  One CTA; deterministic reduction order.
+__global__ void __launch_bounds__(kPrologueThreads)
+adam_prologue(const hm_group_launch* __restrict__ groups, int n_groups,
+              hm_group_rt* __restrict__ rt, hm_adam_hyper hyper,
+              const float* __restrict__ bc_table, int64_t bc_len, int64_t explicit_step,
+              int32_t* __restrict__ steps, uint32_t* __restrict__ applied,
+              uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq, int consume) {
+  __shared__ double red[kPrologueThreads / 32];
+  __shared__ float s_gscale;
+  const bool clip = hyper.max_norm > 0.f && sumsq != nullptr;
+  if (clip) {
+    double local = 0.0;
+    for (int i = threadIdx.x; i < n_groups; i += blockDim.x) {
+      const uint32_t f = groups[i].flag;
+      if (nonfinite == nullptr || nonfinite[f] == 0) local += sumsq[f];
+    }
+    const double total = block_sum<kPrologueThreads>(local, red);
+    if (threadIdx.x == 0) {
+      // Norm of the unscaled gradient; clip coefficient as in common practice.
+      const double norm = sqrt(total) * (double)hyper.inv_scale;
+      const double coef = norm > (double)hyper.max_norm ? (double)hyper.max_norm / (norm + 1e-6) : 1.0;
+      s_gscale = __fmul_rn(hyper.inv_scale, (float)coef);
+    }
+  } else if (threadIdx.x == 0) {
+    s_gscale = hyper.inv_scale;
+  }
+  __syncthreads();
+  const float gscale = s_gscale;
+  for (int i = threadIdx.x; i < n_groups; i += blockDim.x) {
+    const hm_group_launch gl = groups[i];
+    const bool finite = nonfinite == nullptr || nonfinite[gl.flag] == 0;
+    int64_t s;
+    if (explicit_step > 0) {
+      s = 0;  // bc_table[0] holds the caller's step
+    } else {
+      s = (int64_t)steps[gl.group] + 1;
+      if (finite) steps[gl.group] = (int32_t)s;
+      if (s >= bc_len) s = bc_len - 1;  // table is extended until it saturates at 1.0f
+    }
+    hm_group_rt r;
+    r.bc1 = bc_table[2 * s];
+    r.bc2 = bc_table[2 * s + 1];
+    r.gscale = gscale;
+    r.apply = finite ? 1u : 0u;
+    rt[i] = r;
+    if (applied) applied[gl.group] = r.apply;
+    if (consume) {
+      if (nonfinite) nonfinite[gl.flag] = 0u;
+      if (sumsq) sumsq[gl.flag] = 0.0;
+    }
+  }
+}
+
+struct AdamScalars {
+  float lr, b1, ob1, b2, ob2, eps, bc1, bc2, gscale;
+};
+
+__device__ __forceinline__ void adam_elem(const AdamScalars& s, float g, float& p, float& m,
+                                          float& v) {
+  g = __fmul_rn(g, s.gscale);  // x * 1.0f == x exactly: identity for parity runs
+  m = __fadd_rn(__fmul_rn(s.b1, m), __fmul_rn(s.ob1, g));
+  v = __fadd_rn(__fmul_rn(s.b2, v), __fmul_rn(s.ob2, __fmul_rn(g, g)));
+  const float mh = __fdiv_rn(m, s.bc1);
+  const float vh = __fdiv_rn(v, s.bc2);
+  const float den = __fadd_rn(__fsqrt_rn(vh), s.eps);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(s.lr, mh), den));
+}
+
+template <int GDT, int PDT>
+__global__ void __launch_bounds__(kThreads)
+adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ groups,
+          const hm_group_rt* __restrict__ rt, const void* __restrict__ g,
+          float* __restrict__ p32, float* __restrict__ m32, float* __restrict__ v32,
+          void* __restrict__ p16, hm_adam_hyper hyper) {
+  const hm_adam_chunk c = chunks[blockIdx.x];
+  const hm_group_launch gl = groups[c.slot];
+  const hm_group_rt r = rt[c.slot];
+  const uint64_t go = c.g_off + gl.g_shift;
+  const uint64_t so = c.s_off;
+  const uint64_t po = c.p_off + gl.p_shift;
+  const uint32_t n = c.n;
+  const int tid = threadIdx.x;
+  constexpr bool kPub = PDT != 0;
+
+  if (!r.apply) {
+    // Rejected layer: state untouched; still publish the unchanged masters.
+    if constexpr (kPub) {
+      for (uint32_t i = tid; i < n; i += kThreads) store1<PDT>(p16, po + i, p32[so + i]);
+    }
+    return;
+  }
+  AdamScalars s;
+  s.lr = hyper.lr;
+  s.b1 = hyper.beta1;
+  s.ob1 = hyper.one_minus_beta1;
+  s.b2 = hyper.beta2;
+  s.ob2 = hyper.one_minus_beta2;
+  s.eps = hyper.eps;
+  s.bc1 = r.bc1;
+  s.bc2 = r.bc2;
+  s.gscale = r.gscale;
+
+  const bool vec = ((go | so | po | (uint64_t)n) & (kVec - 1)) == 0;
+  if (vec) {
+    // Issue every load of the thread's 2 granules before any math: 2 x
+    // (16 B g + 3 x 32 B state) in flight per thread.
+    F8 gv[kVecPerThread], pv[kVecPerThread], mv[kVecPerThread], vv[kVecPerThread];
+    bool live[kVecPerThread];
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      live[k] = e < n;
+      if (live[k]) {
+        load8_ro<GDT>(g, go + e, gv[k]);
+        load8_rw<HM_DT_F32>(p32, so + e, pv[k]);
+        load8_rw<HM_DT_F32>(m32, so + e, mv[k]);
+        load8_rw<HM_DT_F32>(v32, so + e, vv[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      if (!live[k]) continue;
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) adam_elem(s, gv[k].v[j], pv[k].v[j], mv[k].v[j], vv[k].v[j]);
+      store8<HM_DT_F32>(p32, so + e, pv[k]);
+      store8<HM_DT_F32>(m32, so + e, mv[k]);
+      store8<HM_DT_F32>(v32, so + e, vv[k]);
+      if constexpr (kPub) store8<PDT>(p16, po + e, pv[k]);
+    }
+  } else {
+    for (uint32_t i = tid; i < n; i += kThreads) {
+      float gg = load1<GDT>(g, go + i);
+      float p = p32[so + i], m = m32[so + i], v = v32[so + i];
+      adam_elem(s, gg, p, m, v);
+      p32[so + i] = p;
+      m32[so + i] = m;
+      v32[so + i] = v;
+      if constexpr (kPub) store1<PDT>(p16, po + i, p);
+    }
+  }
+}
+
+using AdamFn = void (*)(const hm_adam_chunk*, const hm_group_launch*, const hm_group_rt*,
+                        const void*, float*, float*, float*, void*, hm_adam_hyper);
+
+template <int GDT>
+AdamFn pick_p(int pdt) {
+  switch (pdt) {
+    case 0: return adam_main<GDT, 0>;
+    case HM_DT_F16: return adam_main<GDT, HM_DT_F16>;
+    case HM_DT_BF16: return adam_main<GDT, HM_DT_BF16>;
+  }
+  return nullptr;
+}
+
+AdamFn pick_adam(int gdt, int pdt) {
+  switch (gdt) {
+    case HM_DT_F16: return pick_p<HM_DT_F16>(pdt);
+    case HM_DT_BF16: return pick_p<HM_DT_BF16>(pdt);
+    case HM_DT_F32: return pick_p<HM_DT_F32>(pdt);
+  }
+  return nullptr;
+}
+
+}  // namespace
+}  // namespace hm
+
+extern "C" int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
+                            const hm_group_launch* groups, int32_t n_groups,
+                            hm_group_rt* rt_scratch, const void* g, int g_dtype, float* p32,
+                            float* m32, float* v32, void* p16, int p16_dtype,
+                            const hm_adam_hyper* hyper, const float* bc_table, int64_t bc_len,
+                            int64_t explicit_step, int32_t* steps, uint32_t* applied,
+                            uint32_t* nonfinite, double* sumsq, int consume_flags,
+                            void* stream) {
+  if (!hyper || !bc_table || bc_len < 1 || !rt_scratch)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: missing hyper/bc_table/rt scratch");
+  if (n_groups <= 0 || n_chunks < 0)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: bad sizes (%d groups, %lld chunks)",
+                        (int)n_groups, (long long)n_chunks);
+  if (explicit_step <= 0 && !steps)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: steps[] required without explicit_step");
+  const int pdt = p16 ? p16_dtype : 0;
+  hm::AdamFn fn = hm::pick_adam(g_dtype, pdt);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_step: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
+  if (n_chunks > 0x7fffffffLL)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: too many chunks (%lld)", (long long)n_chunks);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  hm::adam_prologue<<<1, hm::kPrologueThreads, 0, st>>>(groups, n_groups, rt_scratch, *hyper,
+                                                        bc_table, bc_len, explicit_step, steps,
+                                                        applied, nonfinite, sumsq, consume_flags);
+  HM_CUDA_CHECK_LAUNCH();
+  if (n_chunks > 0) {
+    fn<<<(unsigned)n_chunks, hm::kThreads, 0, st>>>(chunks, groups, rt_scratch, g, p32, m32, v32,
+                                                    p16, *hyper);
+    HM_CUDA_CHECK_LAUNCH();
+  }
+  return HM_OK;
+}

@@ -1,0 +1,338 @@
+// Segment kernels around the fused update:
+//   hm_accumulate   ParamBuffer.accumulate (hiermem/lockfree.py:210-224) with the
+//                   layer's reject flag and grad-norm term fused into the pass (K3)
+//   hm_cast         publish cast (lockfree.py:169) / take widen (lockfree.py:234)
+//   hm_reduce_stats isfinite + f64 sums (lockfree.py:133, 218-237) as a read-only pass
+//   hm_copy_runs    page pack / unpack / relocation (pagemem.py:303-407 data motion, K1)
+//   hm_memcpy_runs  pinned-host <-> HBM page swap on copy engines (K8)
+#include "hm_device.cuh"
+#include "hm_error.h"
+
+namespace hm {
+namespace {
+
+__device__ __forceinline__ void flush_stats(bool bad, double sq, uint32_t* nonfinite, double* sumsq,
+                                            uint32_t slot, double* red) {
+  if (nonfinite) {
+    const int any = __syncthreads_or(bad ? 1 : 0);
+    if (any && threadIdx.x == 0) atomicOr(&nonfinite[slot], 1u);
+  }
+  if (sumsq) {
+    const double tot = block_sum<kThreads>(sq, red);
+    if (threadIdx.x == 0 && tot != 0.0) atomicAdd(&sumsq[slot], tot);
+  }
+}
+
+// dst = rn(f32(dst) + f32(src)) (add) or rn(0.0f + f32(src)) (first message).
+// sumsq accumulates sum(new^2 - old^2) so that it telescopes to the squared
+// norm of the final buffer over any number of messages.
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(kThreads)
+accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
+                  void* __restrict__ dst, int add, uint32_t* __restrict__ nonfinite,
+                  double* __restrict__ sumsq) {
+  __shared__ double red[kThreads / 32];
+  const hm_seg_chunk c = chunks[blockIdx.x];
+  const int tid = threadIdx.x;
+  bool bad = false;
+  double sq = 0.0;
+  const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
+  if (vec) {
+    F8 a[kVecPerThread], b[kVecPerThread];
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e < c.n) {
+        load8_ro<SDT>(src, c.src_off + e, a[k]);
+        if (add) load8_rw<DDT>(dst, c.dst_off + e, b[k]);
+        else {
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) b[k].v[j] = 0.0f;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e >= c.n) continue;
+      F8 o;
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b[k].v[j], a[k].v[j])));
+        bad |= !is_finite(r);
+        if (sumsq) sq += (double)r * (double)r - (double)b[k].v[j] * (double)b[k].v[j];
+        o.v[j] = r;
+      }
+      store8<DDT>(dst, c.dst_off + e, o);
+    }
+  } else {
+    for (uint32_t i = tid; i < c.n; i += kThreads) {
+      const float a1 = load1<SDT>(src, c.src_off + i);
+      const float b1 = add ? load1<DDT>(dst, c.dst_off + i) : 0.0f;
+      const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b1, a1)));
+      bad |= !is_finite(r);
+      if (sumsq) sq += (double)r * (double)r - (double)b1 * (double)b1;
+      store1<DDT>(dst, c.dst_off + i, r);
+    }
+  }
+  flush_stats(bad, sq, nonfinite, sumsq, c.slot, red);
+}
+
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(kThreads)
+cast_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
+            void* __restrict__ dst) {
+  const hm_seg_chunk c = chunks[blockIdx.x];
+  const int tid = threadIdx.x;
+  const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
+  if (vec) {
+    F8 a[kVecPerThread];
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e < c.n) load8_ro<SDT>(src, c.src_off + e, a[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e < c.n) store8<DDT>(dst, c.dst_off + e, a[k]);
+    }
+  } else {
+    for (uint32_t i = tid; i < c.n; i += kThreads)
+      store1<DDT>(dst, c.dst_off + i, load1<SDT>(src, c.src_off + i));
+  }
+}
+
+template <int SDT>
+__global__ void __launch_bounds__(kThreads)
+reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
+              uint32_t* __restrict__ nonfinite, double* __restrict__ sums,
+              double* __restrict__ sumsq) {
+  __shared__ double red[kThreads / 32];
+  const hm_seg_chunk c = chunks[blockIdx.x];
+  const int tid = threadIdx.x;
+  bool bad = false;
+  double s = 0.0, sq = 0.0;
+  const bool vec = ((c.src_off | (uint64_t)c.n) & (kVec - 1)) == 0;
+  if (vec) {
+    F8 a[kVecPerThread];
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e < c.n) load8_ro<SDT>(src, c.src_off + e, a[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e >= c.n) continue;
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const float x = a[k].v[j];
+        bad |= !is_finite(x);
+        s += (double)x;
+        sq += (double)x * (double)x;
+      }
+    }
+  } else {
+    for (uint32_t i = tid; i < c.n; i += kThreads) {
+      const float x = load1<SDT>(src, c.src_off + i);
+      bad |= !is_finite(x);
+      s += (double)x;
+      sq += (double)x * (double)x;
+    }
+  }
+  if (sums) {
+    const double tot = block_sum<kThreads>(s, red);
+    if (threadIdx.x == 0) atomicAdd(&sums[c.slot], tot);
+  }
+  flush_stats(bad, sq, nonfinite, sumsq, c.slot, red);
+}
+
+// Byte-run copy: one CTA per descriptor; 16-byte vectors once source and
+// destination are co-aligned, 4/2/1-byte granules otherwise.
+__global__ void __launch_bounds__(kThreads)
+copy_runs_kernel(const char* __restrict__ src, char* __restrict__ dst,
+                 const hm_copy_desc* __restrict__ descs) {
+  const hm_copy_desc d = descs[blockIdx.x];
+  const char* s = src + d.src_off;
+  char* t = dst + d.dst_off;
+  uint64_t n = d.bytes;
+  const int tid = threadIdx.x;
+  const uint64_t mis = ((uint64_t)s ^ (uint64_t)t);
+  if ((mis & 15) == 0) {
+    const uint64_t head = (16 - ((uint64_t)s & 15)) & 15;
+    const uint64_t h = head < n ? head : n;
+    if ((uint64_t)tid < h) t[tid] = s[tid];
+    s += h;
+    t += h;
+    n -= h;
+    const uint64_t nv = n >> 4;
+    const uint4* sv = reinterpret_cast<const uint4*>(s);
+    uint4* tv = reinterpret_cast<uint4*>(t);
+    uint64_t i = tid;
+    for (; i + 3 * kThreads < nv; i += 4 * kThreads) {
+      uint4 a0 = ld_stream_u4(sv + i), a1 = ld_stream_u4(sv + i + kThreads);
+      uint4 a2 = ld_stream_u4(sv + i + 2 * kThreads), a3 = ld_stream_u4(sv + i + 3 * kThreads);
+      st_stream_u4(tv + i, a0);
+      st_stream_u4(tv + i + kThreads, a1);
+      st_stream_u4(tv + i + 2 * kThreads, a2);
+      st_stream_u4(tv + i + 3 * kThreads, a3);
+    }
+    for (; i < nv; i += kThreads) st_stream_u4(tv + i, ld_stream_u4(sv + i));
+    for (uint64_t j = (nv << 4) + tid; j < n; j += kThreads) t[j] = s[j];
+  } else if ((mis & 3) == 0) {
+    const uint64_t head = (4 - ((uint64_t)s & 3)) & 3;
+    const uint64_t h = head < n ? head : n;
+    if ((uint64_t)tid < h) t[tid] = s[tid];
+    s += h;
+    t += h;
+    n -= h;
+    const uint64_t nw = n >> 2;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(s);
+    uint32_t* tw = reinterpret_cast<uint32_t*>(t);
+    for (uint64_t i = tid; i < nw; i += kThreads) tw[i] = sw[i];
+    for (uint64_t j = (nw << 2) + tid; j < n; j += kThreads) t[j] = s[j];
+  } else if ((mis & 1) == 0) {
+    const uint64_t h = ((uint64_t)s & 1) && n ? 1 : 0;
+    if ((uint64_t)tid < h) t[0] = s[0];
+    s += h;
+    t += h;
+    n -= h;
+    const uint64_t nh = n >> 1;
+    const uint16_t* sh = reinterpret_cast<const uint16_t*>(s);
+    uint16_t* th = reinterpret_cast<uint16_t*>(t);
+    for (uint64_t i = tid; i < nh; i += kThreads) th[i] = sh[i];
+    if ((n & 1) && tid == 0) t[n - 1] = s[n - 1];
+  } else {
+    for (uint64_t j = tid; j < n; j += kThreads) t[j] = s[j];
+  }
+}
+
+
+using AccFn = void (*)(const hm_seg_chunk*, const void*, void*, int, uint32_t*, double*);
+using CastFn = void (*)(const hm_seg_chunk*, const void*, void*);
+using RedFn = void (*)(const hm_seg_chunk*, const void*, uint32_t*, double*, double*);
+
+template <int S>
+AccFn acc_d(int d) {
+  switch (d) {
+    case HM_DT_F16: return accumulate_kernel<S, HM_DT_F16>;
+    case HM_DT_BF16: return accumulate_kernel<S, HM_DT_BF16>;
+    case HM_DT_F32: return accumulate_kernel<S, HM_DT_F32>;
+  }
+  return nullptr;
+}
+AccFn pick_acc(int s, int d) {
+  switch (s) {
+    case HM_DT_F16: return acc_d<HM_DT_F16>(d);
+    case HM_DT_BF16: return acc_d<HM_DT_BF16>(d);
+    case HM_DT_F32: return acc_d<HM_DT_F32>(d);
+  }
+  return nullptr;
+}
+template <int S>
+CastFn cast_d(int d) {
+  switch (d) {
+    case HM_DT_F16: return cast_kernel<S, HM_DT_F16>;
+    case HM_DT_BF16: return cast_kernel<S, HM_DT_BF16>;
+    case HM_DT_F32: return cast_kernel<S, HM_DT_F32>;
+  }
+  return nullptr;
+}
+CastFn pick_cast(int s, int d) {
+  switch (s) {
+    case HM_DT_F16: return cast_d<HM_DT_F16>(d);
+    case HM_DT_BF16: return cast_d<HM_DT_BF16>(d);
+    case HM_DT_F32: return cast_d<HM_DT_F32>(d);
+  }
+  return nullptr;
+}
+RedFn pick_red(int s) {
+  switch (s) {
+    case HM_DT_F16: return reduce_kernel<HM_DT_F16>;
+    case HM_DT_BF16: return reduce_kernel<HM_DT_BF16>;
+    case HM_DT_F32: return reduce_kernel<HM_DT_F32>;
+  }
+  return nullptr;
+}
+
+int check_grid(int64_t n, const char* who) {
+  if (n < 0 || n > 0x7fffffffLL)
+    return hm_set_error(HM_ERR_INVALID, "%s: bad chunk count %lld", who, (long long)n);
+  return HM_OK;
+}
+
+}  // namespace
+}  // namespace hm
+
+extern "C" {
+
+int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
+                  const hm_seg_chunk* chunks, int64_t n_chunks, int mode, uint32_t* nonfinite,
+                  double* sumsq, void* stream) {
+  if (int rc = hm::check_grid(n_chunks, "hm_accumulate")) return rc;
+  hm::AccFn fn = hm::pick_acc(src_dtype, dst_dtype);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_accumulate: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
+  if (n_chunks == 0) return HM_OK;
+  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      chunks, src, dst, mode ? 1 : 0, nonfinite, sumsq);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_cast(const void* src, int src_dtype, void* dst, int dst_dtype, const hm_seg_chunk* chunks,
+            int64_t n_chunks, void* stream) {
+  if (int rc = hm::check_grid(n_chunks, "hm_cast")) return rc;
+  hm::CastFn fn = hm::pick_cast(src_dtype, dst_dtype);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_cast: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
+  if (n_chunks == 0) return HM_OK;
+  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, dst);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_reduce_stats(const void* src, int src_dtype, const hm_seg_chunk* chunks, int64_t n_chunks,
+                    uint32_t* nonfinite, double* sums, double* sumsq, void* stream) {
+  if (int rc = hm::check_grid(n_chunks, "hm_reduce_stats")) return rc;
+  hm::RedFn fn = hm::pick_red(src_dtype);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_reduce_stats: unsupported dtype %d", src_dtype);
+  if (n_chunks == 0) return HM_OK;
+  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, nonfinite,
+                                                                                 sums, sumsq);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_copy_runs(const void* src, void* dst, const hm_copy_desc* descs, int64_t n_descs,
+                 void* stream) {
+  if (int rc = hm::check_grid(n_descs, "hm_copy_runs")) return rc;
+  if (n_descs == 0) return HM_OK;
+  hm::copy_runs_kernel<<<(unsigned)n_descs, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const char*>(src), static_cast<char*>(dst), descs);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_memcpy_runs(const void* src, void* dst, const hm_copy_desc* descs, int64_t n_descs,
+                   int kind, void* stream) {
+  if (n_descs < 0 || (n_descs > 0 && !descs))
+    return hm_set_error(HM_ERR_INVALID, "hm_memcpy_runs: bad descriptors");
+  cudaMemcpyKind k;
+  switch (kind) {
+    case 1: k = cudaMemcpyHostToDevice; break;
+    case 2: k = cudaMemcpyDeviceToHost; break;
+    case 3: k = cudaMemcpyDeviceToDevice; break;
+    default: return hm_set_error(HM_ERR_INVALID, "hm_memcpy_runs: bad kind %d", kind);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int64_t i = 0; i < n_descs; ++i) {
+    const hm_copy_desc& d = descs[i];
+    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + d.dst_off,
+                                    static_cast<const char*>(src) + d.src_off, d.bytes, k, st);
+    if (e != cudaSuccess)
+      return hm_set_error(HM_ERR_CUDA, "hm_memcpy_runs: %s", cudaGetErrorString(e));
+  }
+  return HM_OK;
+}
+
+}  // extern "C"

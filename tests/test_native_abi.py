@@ -1,0 +1,38 @@
+"""The C-ABI library loads without a GPU and exports every function that
+include/hm_page.h declares; the ctypes table covers exactly that set."""
+import ctypes
+import re
+
+from conftest import ROOT
+from paper_2303_02868_b200 import _native as N
+
+
+def declared_functions():
+    text = (ROOT / "include" / "hm_page.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    names = set(re.findall(r"\b(hm_[a-z0-9_]+)\s*\(", text))
+    return names
+
+
+def test_library_exports_header():
+    lib = ctypes.CDLL(str(N.LIB_PATH))
+    names = declared_functions()
+    assert len(names) >= 20
+    for name in sorted(names):
+        assert hasattr(lib, name), f"{name} declared in include/hm_page.h but not exported"
+    assert names == set(N.SIGNATURES), names ^ set(N.SIGNATURES)
+
+
+def test_abi_constants():
+    lib = N.lib()
+    assert lib.hm_abi_version() == 1
+    assert lib.hm_device_chunk_elems() == 4096
+
+
+def test_struct_layouts_match_header():
+    text = (ROOT / "include" / "hm_page.h").read_text()
+    assert "#define HM_ADAM_CHUNK 4096" in text
+    assert N.ADAM_CHUNK.names == ("g_off", "s_off", "p_off", "n", "slot")
+    assert N.GROUP_LAUNCH.names == ("g_shift", "p_shift", "group", "flag")
+    assert N.SEG_CHUNK.names == ("src_off", "dst_off", "n", "slot")
+    assert ctypes.sizeof(N.AdamHyperC) == 32
