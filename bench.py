@@ -1,0 +1,367 @@
+"""Benchmark of the page-granular update hot path (BASELINE.json metric:
+"page-Adam params/s + HBM GB/s; page RS/AG bus GB/s at 1/2/4/8 B200").
+
+One *step* = one fused page sweep of the updating actor over every layer of
+the workload (hiermem/lockfree.py:624-639: take -> update_layer ->
+publish), i.e. prologue + page-Adam over all param pages: 28 B/param of HBM
+traffic.  At N>1 a step is the data-parallel page step: gradient
+reduce-scatter over the page pool, the sharded sweep, parameter all-gather.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--dtype bf16]
+    python bench.py --impl reference ...     # the reference CPU path (oracle port)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_PARAM = 28  # read g16 2 + p/m/v 12; write p/m/v 12 + p16 2
+METRIC = "page-Adam params/s + HBM GB/s; page RS/AG bus GB/s at 1/2/4/8 B200"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---- clocks sampling during the timed region -------------------------------------
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int = 0, period_ms: int = 20):
+        self.index, self.period_ms = index, period_ms
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", f"-lms", str(self.period_ms)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                bits = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx = m
+            for b, name in REASON_BITS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- CPU baseline (oracle port of the reference, bounded sample) ---------------------
+
+def cpu_reference_sample(specs, page_bytes, sample_pages: int, threads: int, dtype: str, reps: int):
+    """Time the reference chain take -> apply_update -> publish cast, restated
+    op-for-op in numpy (oracle/page_adam.py, pinned to the reference), over
+    the first ``sample_pages`` pages' worth of parameters of the workload,
+    fanned out over ``threads`` host threads (numpy ufuncs release the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import page_adam as O
+    E = page_bytes // 2
+    n = sample_pages * E
+    p, m, v, g16 = O.synthetic_layer(0, 0, n, dtype, outliers=False)
+    pieces = np.array_split(np.arange(n), threads * 4)
+    bounds = [(int(a[0]), int(a[-1]) + 1) for a in pieces if len(a)]
+
+    def work(b):
+        lo, hi = b
+        g = O.from16(g16[lo:hi], dtype)                                       # take (widen)
+        pp, mm, vv, ok = O.adam_update(p[lo:hi], m[lo:hi], v[lo:hi], g, 1e-3, 0.9, 0.999, 1e-8, 10)
+        O.publish16(pp, dtype)                                              # publish cast
+        return ok
+
+    best = float("inf")
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(work, bounds))  # warm
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            list(ex.map(work, bounds))
+            best = min(best, time.perf_counter() - t0)
+    return n, best
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU update path on the host cores."""
+    from paper_2303_02868_b200 import workloads as W
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    specs = W.config_specs(args.config)
+    page = args.page_mib * 2**20 if args.page_mib else W.config_page_bytes(args.config)
+    threads = os.cpu_count() or 1
+    E = page // 2
+    sample_pages = max(1, min(args.cpu_sample_pages, sum(s.bytes for s in specs) // page))
+    times = []
+    n = sample_pages * E
+    for i in range(args.warmup + args.steps):
+        nn, t = cpu_reference_sample(specs, page, sample_pages, threads, args.dtype, reps=1)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    value = n / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "params/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "page_bytes": page,
+                   "params": W.total_elems(specs), "grad_dtype": args.dtype},
+        "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads, "kind": "port",
+                         "sample": f"first {sample_pages} pages ({n} params) of the {args.config} pool per step; "
+                                   "take->apply_update->publish restated op-for-op in numpy "
+                                   "(oracle/page_adam.py, bit-exact to hiermem/lockfree.py:127-263)"},
+        "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- the GPU arm ----------------------------------------------------------------------
+
+def build_state(args, device, world=1, rank=0):
+    import torch
+    from paper_2303_02868_b200 import lockfree as LF
+    from paper_2303_02868_b200 import workloads as W
+    from paper_2303_02868_b200.layout import PageLayout
+    specs = W.config_specs(args.config)
+    page = args.page_mib * 2**20 if args.page_mib else W.config_page_bytes(args.config)
+    numels = [s.bytes // 2 for s in specs]
+    layout = PageLayout(numels, page, world_size=world, rank=rank,
+                        bucket_pages=args.bucket_pages if world > 1 else None,
+                        names=[s.name for s in specs])
+    gen = torch.Generator(device=device)
+    gen.manual_seed(1234)
+    params = [torch.empty(n, dtype=torch.float32, device=device).normal_(0, 0.02, generator=gen)
+              for n in numels]
+    buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout)
+    ms = LF.MasterState(params, page_bytes=page, device=device, layout=layout)
+    del params
+    torch.cuda.empty_cache()
+    return specs, page, layout, buf, ms
+
+
+def synthetic_grads(numels, dtype, device, seed):
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+    return [torch.empty(n, dtype=torch.float32, device=device).normal_(0, 1e-2, generator=gen).to(tdt)
+            for n in numels]
+
+
+def run_ours_single(args):
+    import torch
+    from paper_2303_02868_b200 import lockfree as LF
+    from paper_2303_02868_b200 import workloads as W
+    device = torch.device("cuda", 0)
+    torch.cuda.set_device(device)
+    specs, page, layout, buf, ms = build_state(args, device)
+    L = len(specs)
+    numels = layout.numels
+    P = sum(numels)
+    hyper = LF.AdamHyper(lr=1e-3)
+    # Fill BOTH gradient page buffers through accumulate (K3, which also
+    # computes each layer's finite flag); every step re-offers them, so the
+    # timed region reads gradients already resident in HBM.
+    grads = synthetic_grads(numels, args.dtype, device, 7)
+    for rnd in range(2):
+        for l in range(L):
+            buf.accumulate(LF.GradMessage(l, grads[l], rnd))
+        if rnd == 0:
+            LF.sweep(buf, ms, hyper)
+
+    def rearm():
+        for l in range(L):
+            buf._pending[l] = 1
+
+    stream = torch.cuda.current_stream(device)
+    for _ in range(args.warmup):
+        rearm()
+        LF.sweep(buf, ms, hyper)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    with ClockSampler(0) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(args.steps):
+            rearm()
+            ev[2 * i].record(stream)
+            LF.sweep(buf, ms, hyper)
+            ev[2 * i + 1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    kern_ms = statistics.mean(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps))
+    ms_per_step = total_ms / args.steps
+    value = P / (ms_per_step / 1e3)
+    peak, peak_kind = load_peaks()
+    achieved = BYTES_PER_PARAM * P / (kern_ms / 1e3) / 1e9
+
+    # K3 producer throughput (accumulate into pages, fused finite flag + norm).
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for l in range(L):
+        buf._pending[l] = 0
+    a0.record(stream)
+    for l in range(L):
+        buf.accumulate(LF.GradMessage(l, grads[l], 0))
+    a1.record(stream)
+    torch.cuda.synchronize()
+    acc_ms = a0.elapsed_time(a1)
+    LF.sweep(buf, ms, hyper)
+
+    e2e = run_e2e(args, buf, ms, hyper, grads, device) if args.e2e_steps > 0 else None
+    traffic = load_traffic(args)
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n, t = cpu_reference_sample(specs, page, args.cpu_sample_pages, threads, args.dtype, reps=2)
+        cpu = {"value": n / t, "unit": "params/s", "cores": threads, "kind": "port",
+               "sample": f"first {args.cpu_sample_pages} pages ({n} params) of the {args.config} pool; "
+                         "take->apply_update->publish restated op-for-op in numpy (oracle/page_adam.py), "
+                         f"{threads} threads, best of 2"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": P,
+                   "layers": L, "page_bytes": page, "pages": layout.used_pages,
+                   "l2": "inputs larger than L2 (28 B/param x params >> 126 MB)",
+                   "step": "fused sweep: prologue + page-Adam over all pages (take->update->publish)"},
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+                     "bytes_per_param": BYTES_PER_PARAM, "kernel": "adam_main (+ prologue)",
+                     "kernel_ms": kern_ms},
+        "accumulate": {"params_per_s": P / (acc_ms / 1e3), "ms": acc_ms,
+                       "gbs": 4 * P / (acc_ms / 1e3) / 1e9, "bytes_per_param": 4,
+                       "note": "K3: first-message accumulate (read payload, write page) with fused "
+                               "finite flag + squared norm, one launch per layer"},
+        "clocks": clk.summary(),
+        "gpu_launches": 2 * args.steps,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, buf, ms, hyper, grads, device):
+    """Public API with host buffers: per step H2D of every layer's gradient
+    from pinned memory + accumulate (K3) + fused sweep (K2) + D2H of the
+    per-layer applied flags (the step's result)."""
+    import torch
+    from paper_2303_02868_b200 import lockfree as LF
+    host = [g.cpu().pin_memory() for g in grads]
+    h2d = sum(h.numel() * h.element_size() for h in host)
+    L = len(host)
+
+    def step():
+        for l in range(L):
+            buf.accumulate(LF.GradMessage(l, host[l], 0))
+        res = LF.sweep(buf, ms, hyper)
+        return res.applied()
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    P = sum(buf.layout.numels)
+    return {"value": P / dt, "unit": "params/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": 4 * L, "ms_per_step": dt * 1e3, "steps": args.e2e_steps}
+
+
+def load_traffic(args):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d.get(f"{args.config}:{args.dtype}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--page-mib", type=int, default=0)
+    ap.add_argument("--bucket-pages", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample-pages", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2303_02868_b200 import dp_bench
+        return dp_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks)
+    return run_ours_single(args)
+
+
+if __name__ == "__main__":
+    main()

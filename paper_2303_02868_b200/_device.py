@@ -1,0 +1,208 @@
+"""Device plumbing: torch owns device memory and streams; this module turns
+tensors into raw pointers for the C-ABI, caches descriptor uploads, and
+holds the exact bias-correction tables.  No compute happens here."""
+from __future__ import annotations
+
+import ctypes as C
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import NativeError
+
+TORCH16 = {"fp16": torch.float16, "bf16": torch.bfloat16}
+DT_OF_TORCH = {torch.float16: N.DT_F16, torch.bfloat16: N.DT_BF16, torch.float32: N.DT_F32}
+F32 = np.float32
+
+
+def require_device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise NativeError("a CUDA device is required: the page-update path has no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise NativeError(f"device {d} is not a CUDA device (no CPU fallback)")
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def cur_stream(device, stream=None):
+    return stream if stream is not None else torch.cuda.current_stream(device)
+
+
+def sptr(stream) -> C.c_void_p:
+    return C.c_void_p(int(stream.cuda_stream))
+
+
+class DescCache:
+    """Device copies of host descriptor arrays.  Static plans are keyed by the
+    identity of the (cached, immortal) numpy array; per-launch tables by their
+    bytes in a small LRU, so steady-state sweeps upload nothing."""
+
+    def __init__(self, device, lru: int = 64):
+        self.device = device
+        self._static: dict[int, tuple[np.ndarray, torch.Tensor]] = {}
+        self._lru: OrderedDict[bytes, torch.Tensor] = OrderedDict()
+        self._lru_cap = lru
+
+    def static(self, arr: np.ndarray) -> torch.Tensor:
+        hit = self._static.get(id(arr))
+        if hit is not None and hit[0] is arr:
+            return hit[1]
+        dev = self._upload(arr)
+        self._static[id(arr)] = (arr, dev)
+        return dev
+
+    def table(self, arr: np.ndarray) -> torch.Tensor:
+        key = arr.tobytes()
+        dev = self._lru.get(key)
+        if dev is not None:
+            self._lru.move_to_end(key)
+            return dev
+        dev = self._upload(arr)
+        self._lru[key] = dev
+        if len(self._lru) > self._lru_cap:
+            self._lru.popitem(last=False)
+        return dev
+
+    def _upload(self, arr: np.ndarray) -> torch.Tensor:
+        raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+        if raw.size == 0:
+            return torch.empty(8, dtype=torch.uint8, device=self.device)
+        return torch.from_numpy(raw.copy()).to(self.device)
+
+
+class BiasTable:
+    """f32(1 - beta**step) for step = 0..len-1, computed in Python double
+    exactly as hiermem/lockfree.py:137-140 does (never a device pow).  The
+    sequence is monotone and reaches 1.0f; the table grows lazily to the
+    largest reachable step and stops growing once both columns saturate
+    (the prologue clamps to the last row)."""
+
+    def __init__(self, beta1: float, beta2: float, device):
+        self.beta1, self.beta2 = float(beta1), float(beta2)
+        self.device = device
+        self.rows: list[tuple[float, float]] = [(0.0, 0.0)]
+        self.saturated = False
+        self.dev = None
+
+    def ensure(self, max_step: int) -> tuple[torch.Tensor, int]:
+        target = max_step + 1
+        if (len(self.rows) < target and not self.saturated) or self.dev is None:
+            grow = max(target, 2 * len(self.rows), 64)
+            s = len(self.rows)
+            while s < grow:
+                a, b = F32(1.0 - self.beta1 ** s), F32(1.0 - self.beta2 ** s)
+                self.rows.append((a, b))
+                s += 1
+                if a == F32(1.0) and b == F32(1.0) and s > 1:
+                    self.saturated = True
+                    break
+            self.dev = torch.tensor(np.array(self.rows, dtype=F32).reshape(-1), device=self.device)
+        return self.dev, len(self.rows)
+
+
+def hyper_c(h) -> N.AdamHyperC:
+    """AdamHyper -> f32 scalars with numpy's weak-scalar rounding
+    (lockfree.py:135-141: python float -> f32 per operation)."""
+    return N.AdamHyperC(
+        float(F32(h.lr)), float(F32(h.beta1)), float(F32(1.0 - h.beta1)),
+        float(F32(h.beta2)), float(F32(1.0 - h.beta2)), float(F32(h.eps)),
+        float(F32(getattr(h, "inv_scale", 1.0))), float(F32(getattr(h, "max_norm", 0.0))))
+
+
+def contiguous_chunks(n: int, slot: int = 0) -> np.ndarray:
+    """hm_seg_chunk units covering [0, n) of a contiguous buffer (src == dst)."""
+    full = n // 4096
+    rest = n - full * 4096
+    body = rest - rest % 8
+    offs = [np.arange(full, dtype=np.int64) * 4096]
+    ns = [np.full(full, 4096, dtype=np.int64)]
+    if body:
+        offs.append(np.array([full * 4096]))
+        ns.append(np.array([body]))
+    if rest - body:
+        offs.append(np.array([full * 4096 + body]))
+        ns.append(np.array([rest - body]))
+    o = np.concatenate(offs)
+    a = np.empty(len(o), dtype=N.SEG_CHUNK)
+    a["src_off"] = o
+    a["dst_off"] = o
+    a["n"] = np.concatenate(ns)
+    a["slot"] = slot
+    return a
+
+
+_CONTIG: dict[tuple[int, int], np.ndarray] = {}
+
+
+def contiguous_chunks_cached(n: int, slot: int = 0) -> np.ndarray:
+    key = (n, slot)
+    if key not in _CONTIG:
+        _CONTIG[key] = contiguous_chunks(n, slot)
+    return _CONTIG[key]
+
+
+def contiguous_adam_chunks(n: int) -> np.ndarray:
+    seg = contiguous_chunks_cached(n)
+    a = np.empty(len(seg), dtype=N.ADAM_CHUNK)
+    a["g_off"] = seg["src_off"]
+    a["s_off"] = seg["src_off"]
+    a["p_off"] = seg["src_off"]
+    a["n"] = seg["n"]
+    a["slot"] = 0
+    return a
+
+
+# ---- host <-> device conversion ------------------------------------------------
+
+def _np_bf16():
+    try:
+        import ml_dtypes
+        return ml_dtypes.bfloat16
+    except Exception:  # pragma: no cover
+        return None
+
+
+def to_device_flat(x, device, float_dtype=None) -> torch.Tensor:
+    """Any array-like -> contiguous 1-D CUDA tensor (f16/bf16/f32 kept; f64 and
+    ints rounded to f32 on the host, as numpy's astype(float32) would)."""
+    if isinstance(x, torch.Tensor):
+        t = x.detach()
+        if t.dtype not in DT_OF_TORCH:
+            t = t.to(torch.float32)
+        t = t.reshape(-1)
+        if t.device.type == "cpu":
+            return t.to(device, non_blocking=t.is_pinned()).contiguous()
+        return t.to(device).contiguous()
+    a = np.asarray(x)
+    bf = _np_bf16()
+    if bf is not None and a.dtype == bf:
+        t = torch.from_numpy(np.ascontiguousarray(a).view(np.int16).reshape(-1).copy())
+        return t.view(torch.bfloat16).to(device)
+    if a.dtype not in (np.float16, np.float32):
+        a = a.astype(np.float32)
+    return torch.from_numpy(np.ascontiguousarray(a).reshape(-1).copy()).to(device)
+
+
+def to_host(t: torch.Tensor, shape, readonly: bool = False) -> np.ndarray:
+    if t.dtype == torch.bfloat16:
+        bits = t.view(torch.int16).cpu().numpy().view(np.uint16)
+        bf = _np_bf16()
+        a = bits.view(bf) if bf is not None else bits
+    else:
+        a = t.cpu().numpy()
+    a = a.reshape(shape)
+    if readonly:
+        a.flags.writeable = False
+    return a
+
+
+def check(rc: int) -> None:
+    N.check(rc)
