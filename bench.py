@@ -359,7 +359,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_2303_02868_b200 import dp_bench
-        return dp_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks)
+        return dp_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks, build_state)
     return run_ours_single(args)
 
 

@@ -175,6 +175,18 @@ int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                  uint32_t* nonfinite, double* sumsq, int consume_flags,
                  void* stream);
 
+/* The two halves of hm_adam_step, for callers that pipeline the main pass
+ * (e.g. per all-gather bucket) after ONE prologue over every group: the
+ * prologue must run exactly once per update or steps[] would advance twice. */
+int hm_adam_prologue(const hm_group_launch* groups, int32_t n_groups, hm_group_rt* rt_scratch,
+                     const hm_adam_hyper* hyper, const float* bc_table, int64_t bc_len,
+                     int64_t explicit_step, int32_t* steps, uint32_t* applied,
+                     uint32_t* nonfinite, double* sumsq, int consume_flags, void* stream);
+int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* groups,
+                 const hm_group_rt* rt, const void* g, int g_dtype,
+                 float* p32, float* m32, float* v32, void* p16, int p16_dtype,
+                 const hm_adam_hyper* hyper, void* stream);
+
 /* Elementwise segment chunk used by accumulate / cast / reduce. */
 typedef struct hm_seg_chunk {
   uint64_t src_off;   /* element offset into src */
@@ -189,10 +201,12 @@ typedef struct hm_seg_chunk {
  *                                        buffer; == add onto zeros, bitwise)
  * and, fused into the same pass, nonfinite[slot] |= any(!isfinite(dst)) and
  * sumsq[slot] += sum(dst^2) (f64) — the layer's reject flag
- * (lockfree.py:133) and grad-norm term, so the update never re-reads g. */
+ * (lockfree.py:133) and grad-norm term, so the update never re-reads g.
+ * slot_modes (nullable): per-slot mode overriding `mode`, so one launch can
+ * accumulate a whole flat gradient into many layers' pages. */
 int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
                   const hm_seg_chunk* chunks, int64_t n_chunks, int mode,
-                  uint32_t* nonfinite, double* sumsq, void* stream);
+                  const uint8_t* slot_modes, uint32_t* nonfinite, double* sumsq, void* stream);
 
 /* RNE dtype conversion over segments: publish cast (lockfree.py:169), take
  * widen (lockfree.py:234), pack/unpack of typed tensors. */

@@ -193,6 +193,51 @@ AdamFn pick_adam(int gdt, int pdt) {
 }  // namespace
 }  // namespace hm
 
+namespace {
+int prologue_args_ok(const hm_adam_hyper* hyper, const float* bc_table, int64_t bc_len,
+                     const hm_group_rt* rt, int32_t n_groups, int64_t explicit_step,
+                     const int32_t* steps) {
+  if (!hyper || !bc_table || bc_len < 1 || !rt)
+    return hm_set_error(HM_ERR_INVALID, "adam prologue: missing hyper/bc_table/rt scratch");
+  if (n_groups <= 0)
+    return hm_set_error(HM_ERR_INVALID, "adam prologue: bad group count %d", (int)n_groups);
+  if (explicit_step <= 0 && !steps)
+    return hm_set_error(HM_ERR_INVALID, "adam prologue: steps[] required without explicit_step");
+  return HM_OK;
+}
+}  // namespace
+
+extern "C" int hm_adam_prologue(const hm_group_launch* groups, int32_t n_groups,
+                                hm_group_rt* rt_scratch, const hm_adam_hyper* hyper,
+                                const float* bc_table, int64_t bc_len, int64_t explicit_step,
+                                int32_t* steps, uint32_t* applied, uint32_t* nonfinite,
+                                double* sumsq, int consume_flags, void* stream) {
+  if (int rc = prologue_args_ok(hyper, bc_table, bc_len, rt_scratch, n_groups, explicit_step, steps))
+    return rc;
+  hm::adam_prologue<<<1, hm::kPrologueThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      groups, n_groups, rt_scratch, *hyper, bc_table, bc_len, explicit_step, steps, applied,
+      nonfinite, sumsq, consume_flags);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
+                            const hm_group_launch* groups, const hm_group_rt* rt, const void* g,
+                            int g_dtype, float* p32, float* m32, float* v32, void* p16,
+                            int p16_dtype, const hm_adam_hyper* hyper, void* stream) {
+  if (!hyper || !rt) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: missing hyper/rt");
+  if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_main: bad chunk count %lld", (long long)n_chunks);
+  const int pdt = p16 ? p16_dtype : 0;
+  hm::AdamFn fn = hm::pick_adam(g_dtype, pdt);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
+  if (n_chunks == 0) return HM_OK;
+  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      chunks, groups, rt, g, p32, m32, v32, p16, *hyper);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
 extern "C" int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                             const hm_group_launch* groups, int32_t n_groups,
                             hm_group_rt* rt_scratch, const void* g, int g_dtype, float* p32,
@@ -201,27 +246,13 @@ extern "C" int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                             int64_t explicit_step, int32_t* steps, uint32_t* applied,
                             uint32_t* nonfinite, double* sumsq, int consume_flags,
                             void* stream) {
-  if (!hyper || !bc_table || bc_len < 1 || !rt_scratch)
-    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: missing hyper/bc_table/rt scratch");
-  if (n_groups <= 0 || n_chunks < 0)
-    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: bad sizes (%d groups, %lld chunks)",
-                        (int)n_groups, (long long)n_chunks);
-  if (explicit_step <= 0 && !steps)
-    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: steps[] required without explicit_step");
   const int pdt = p16 ? p16_dtype : 0;
-  hm::AdamFn fn = hm::pick_adam(g_dtype, pdt);
-  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_step: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
-  if (n_chunks > 0x7fffffffLL)
-    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: too many chunks (%lld)", (long long)n_chunks);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  hm::adam_prologue<<<1, hm::kPrologueThreads, 0, st>>>(groups, n_groups, rt_scratch, *hyper,
-                                                        bc_table, bc_len, explicit_step, steps,
-                                                        applied, nonfinite, sumsq, consume_flags);
-  HM_CUDA_CHECK_LAUNCH();
-  if (n_chunks > 0) {
-    fn<<<(unsigned)n_chunks, hm::kThreads, 0, st>>>(chunks, groups, rt_scratch, g, p32, m32, v32,
-                                                    p16, *hyper);
-    HM_CUDA_CHECK_LAUNCH();
-  }
-  return HM_OK;
+  if (!hm::pick_adam(g_dtype, pdt))
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_step: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
+  if (int rc = hm_adam_prologue(groups, n_groups, rt_scratch, hyper, bc_table, bc_len,
+                                explicit_step, steps, applied, nonfinite, sumsq, consume_flags,
+                                stream))
+    return rc;
+  return hm_adam_main(chunks, n_chunks, groups, rt_scratch, g, g_dtype, p32, m32, v32, p16,
+                      p16_dtype, hyper, stream);
 }

@@ -29,10 +29,11 @@ __device__ __forceinline__ void flush_stats(bool bad, double sq, uint32_t* nonfi
 template <int SDT, int DDT>
 __global__ void __launch_bounds__(kThreads)
 accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
-                  void* __restrict__ dst, int add, uint32_t* __restrict__ nonfinite,
-                  double* __restrict__ sumsq) {
+                  void* __restrict__ dst, int mode, const uint8_t* __restrict__ slot_modes,
+                  uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq) {
   __shared__ double red[kThreads / 32];
   const hm_seg_chunk c = chunks[blockIdx.x];
+  const int add = slot_modes ? (int)slot_modes[c.slot] : mode;
   const int tid = threadIdx.x;
   bool bad = false;
   double sq = 0.0;
@@ -209,7 +210,8 @@ copy_runs_kernel(const char* __restrict__ src, char* __restrict__ dst,
 }
 
 
-using AccFn = void (*)(const hm_seg_chunk*, const void*, void*, int, uint32_t*, double*);
+using AccFn = void (*)(const hm_seg_chunk*, const void*, void*, int, const uint8_t*, uint32_t*,
+                       double*);
 using CastFn = void (*)(const hm_seg_chunk*, const void*, void*);
 using RedFn = void (*)(const hm_seg_chunk*, const void*, uint32_t*, double*, double*);
 
@@ -268,14 +270,14 @@ int check_grid(int64_t n, const char* who) {
 extern "C" {
 
 int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
-                  const hm_seg_chunk* chunks, int64_t n_chunks, int mode, uint32_t* nonfinite,
-                  double* sumsq, void* stream) {
+                  const hm_seg_chunk* chunks, int64_t n_chunks, int mode,
+                  const uint8_t* slot_modes, uint32_t* nonfinite, double* sumsq, void* stream) {
   if (int rc = hm::check_grid(n_chunks, "hm_accumulate")) return rc;
   hm::AccFn fn = hm::pick_acc(src_dtype, dst_dtype);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_accumulate: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
   if (n_chunks == 0) return HM_OK;
   fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      chunks, src, dst, mode ? 1 : 0, nonfinite, sumsq);
+      chunks, src, dst, mode ? 1 : 0, slot_modes, nonfinite, sumsq);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }

@@ -1,0 +1,157 @@
+"""bench.py's N>1 arm: the data-parallel page step under torchrun (one
+process per GPU, NCCL over NVLink/NVSwitch).
+
+Step = reduce-scatter of the bf16 gradient page pool (in place, bucketed) ->
+finite/norm check of the owned reduced pages + per-layer flag all-reduce ->
+prologue -> page-Adam per bucket with the parameter all-gather of bucket b
+overlapped with Adam of bucket b+1.  ``value`` = params of the whole model
+updated per second (strong scaling: the model is fixed, each rank updates
+1/N of its pages); RS/AG bus bandwidths are reported beside it,
+busbw = (S/t)(N-1)/N with S the bytes of the full 16-bit pool.
+
+Synthetic gradients: each rank holds non-zero gradients only in the pages it
+owns, so the in-place reduce-scatter returns every owner its own values and
+re-offering the same pages every step keeps them bounded (no growth across
+timed steps); the collective still moves the whole pool.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+
+import torch
+import torch.distributed as dist
+
+
+def _init():
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    return rank, world, torch.device("cuda", local)
+
+
+def owned_grad_flat(layout, dtype, device, seed):
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+    total = sum(layout.numels)
+    flat = torch.zeros(total, dtype=tdt, device=device)
+    base = 0
+    for l, n in enumerate(layout.numels):
+        for s in layout.segments[l]:
+            if layout.owned(s):
+                flat[base + s.pos: base + s.pos + s.n] = torch.empty(
+                    s.n, device=device).normal_(0, 1e-2, generator=gen).to(tdt)
+        base += n
+    return flat
+
+
+def _max_over_ranks(x: float) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
+    from . import lockfree as LF
+    from . import workloads as W
+    from .sharding import ShardedPageStep
+    rank, world, device = _init()
+    specs, page, layout, buf, ms = build_state(args, device, world, rank)
+    L = len(specs)
+    P = sum(layout.numels)
+    hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
+    dp = ShardedPageStep(buf, ms)
+    flat = owned_grad_flat(layout, args.dtype, device, 7 + rank)
+    for rnd in range(2):  # fill both gradient page buffers (K3)
+        buf.accumulate_flat(flat, rnd)
+        if rnd == 0:
+            dp.step(hyper)
+
+    def rearm():
+        for l in range(L):
+            buf._pending[l] = 1
+
+    stream = torch.cuda.current_stream(device)
+    for _ in range(args.warmup):
+        rearm()
+        dp.step(hyper)
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", rank))) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            rearm()
+            dp.step(hyper)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    step_ms = _max_over_ranks(t0.elapsed_time(t1) / args.steps)
+
+    # Component timings (one instrumented step + isolated collectives).
+    rearm()
+    tm = {}
+    dp.step(hyper, timings=tm)
+    torch.cuda.synchronize()
+    mk = tm["_marks"]
+    parts = {"rs_ms": mk["start"].elapsed_time(mk["rs"]), "check_ms": mk["rs"].elapsed_time(mk["check"]),
+             "adam_ms": mk["check"].elapsed_time(mk["adam"]), "ag_tail_ms": mk["adam"].elapsed_time(mk["ag"])}
+    parts = {k: _max_over_ranks(v) for k, v in parts.items()}
+    gpool = buf.g16_pool[buf._gsel[0] ^ 1]
+    ppool = buf.p16_pool[buf._psel[0]]
+    reps = 10
+
+    def timed(fn):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return _max_over_ranks(a.elapsed_time(b) / reps)
+
+    rs_ms = timed(lambda: dp.coll.reduce_scatter(gpool))
+    ag_ms = timed(lambda: dp.coll.all_gather(ppool))
+    pool_bytes = layout.elems16 * 2
+    busbw = lambda ms_: pool_bytes / (ms_ / 1e3) * (world - 1) / world / 1e9
+    # Sharded page-Adam alone (owned pages) for the HBM roofline.
+    owned = layout.owned_numel()
+    adam_ms = _max_over_ranks(parts["adam_ms"])
+    peak, peak_kind = load_peaks()
+    achieved = bytes_per_param * owned / (adam_ms / 1e3) / 1e9 if adam_ms > 0 else None
+    line = {
+        "metric": metric, "value": P / (step_ms / 1e3), "unit": "params/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": P, "layers": L,
+                   "page_bytes": page, "pages": layout.used_pages, "bucket_pages_per_rank": layout.K,
+                   "buckets": layout.num_buckets, "parallelism": f"dp{world} (page-sharded ZeRO-3)",
+                   "l2": "inputs larger than L2",
+                   "step": "RS(grad pages) -> check -> flag all-reduce -> prologue -> "
+                           "page-Adam(bucket) || AG(bucket)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "peak_kind": peak_kind,
+                     "traffic": None, "kernel": "adam_main on owned pages (instrumented step, "
+                                                "overlapped with AG)", "kernel_ms": adam_ms},
+        "nvlink": {"rs_ms": rs_ms, "ag_ms": ag_ms, "rs_busbw_gbs": busbw(rs_ms), "ag_busbw_gbs": busbw(ag_ms),
+                   "peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                   "nominal_gbs": 900.0, "rs_frac": busbw(rs_ms) / 770.0, "ag_frac": busbw(ag_ms) / 770.0,
+                   "pool_bytes": pool_bytes},
+        "components_ms": parts,
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps * (2 + layout.num_buckets),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -134,11 +134,16 @@ class PageLayout:
         return b * span, (b + 1) * span
 
     # -- kernel descriptors --------------------------------------------------
-    def adam_chunks(self, layers, g_source: str = "pool", owned_only: bool = True) -> np.ndarray:
+    def bucket_of(self, pid: int) -> int:
+        return pid // (self.world_size * self.K)
+
+    def adam_chunks(self, layers, g_source: str = "pool", owned_only: bool = True,
+                    bucket: int | None = None) -> np.ndarray:
         """hm_adam_chunk array for the given layers (slot = index in ``layers``).
         g_source="pool": gradient read from the 16-bit pool (fused sweep);
-        "tensor": from a contiguous per-layer gradient tensor (update_layer)."""
-        return _adam_chunks(self, tuple(layers), g_source, owned_only)
+        "tensor": from a contiguous per-layer gradient tensor (update_layer).
+        bucket: restrict to the pages of one all-gather bucket."""
+        return _adam_chunks(self, tuple(layers), g_source, owned_only, bucket)
 
     def seg_chunks(self, layer: int, pool: str, owned_only: bool = False, slot: int = 0,
                    reverse: bool = False) -> np.ndarray:
@@ -153,16 +158,18 @@ class PageLayout:
         return _pool_chunks(self, tuple(layers), pool, owned_only)
 
 
-def _unit_arrays(lay: PageLayout, layer: int, owned_only: bool):
+def _unit_arrays(lay: PageLayout, layer: int, owned_only: bool, bucket: int | None = None):
     """Per layer: (off16, off_state, tensor_pos, n) int64 arrays of kernel units,
     vectorised per segment (few segments, many 4096-element chunks)."""
     cache = lay.__dict__.setdefault("_unit_cache", {})
-    key = (layer, owned_only)
+    key = (layer, owned_only, bucket)
     if key in cache:
         return cache[key]
     o16s, osts, poss, ns = [], [], [], []
     for s in lay.segments[layer]:
         if owned_only and not lay.owned(s):
+            continue
+        if bucket is not None and lay.bucket_of(s.page) != bucket:
             continue
         base16 = lay.slot16(s.page) * lay.E + s.off
         basest = lay.slot_state(s.page) * lay.E + s.off
@@ -202,14 +209,15 @@ def _unit_arrays(lay: PageLayout, layer: int, owned_only: bool):
     return out
 
 
-def _adam_chunks(lay: PageLayout, layers: tuple, g_source: str, owned_only: bool) -> np.ndarray:
+def _adam_chunks(lay: PageLayout, layers: tuple, g_source: str, owned_only: bool,
+                 bucket: int | None = None) -> np.ndarray:
     cache = lay.__dict__.setdefault("_adam_cache", {})
-    key = (layers, g_source, owned_only)
+    key = (layers, g_source, owned_only, bucket)
     if key in cache:
         return cache[key]
     parts = []
     for slot, l in enumerate(layers):
-        o16, ost, pos, n = _unit_arrays(lay, l, owned_only)
+        o16, ost, pos, n = _unit_arrays(lay, l, owned_only, bucket)
         a = np.empty(len(n), dtype=N.ADAM_CHUNK)
         a["g_off"] = pos if g_source == "tensor" else o16
         a["s_off"] = ost

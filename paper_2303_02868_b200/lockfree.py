@@ -442,16 +442,14 @@ class ParamBuffer(_Paged):
         return self._out(out, layer, readonly)
 
     def _pool_sum(self, buf, layer, stream) -> float:
-        """f64 sum of the layer's gradient pages (ledger only)."""
+        """f64 sum of the layer's gradient pages — ConservationLedger only
+        (check-only bookkeeping, never on the update path).  The pages are
+        unpacked by the page kernel and summed with torch's fixed-order
+        reduction so that the same data always yields the same float (the
+        ledger compares sums for equality, lockfree.py:311)."""
+        g = self._unpack16(self.g16_pool[buf], layer, stream=stream)
         with torch.cuda.stream(stream):
-            out = torch.zeros(1, dtype=torch.float64, device=self.device)
-        ch = self.layout.seg_chunks(layer, "16", reverse=True)
-        # reduce over pool offsets: src offsets of the unpack map are pool offsets
-        D.check(N.lib().hm_reduce_stats(D.ptr(self.g16_pool[buf]), self._dt,
-                                         D.ptr(self._eng.desc.static(ch)), len(ch), None,
-                                         D.ptr(out), None, D.sptr(stream)))
-        with torch.cuda.stream(stream):
-            return float(out.item())
+            return float(torch.as_tensor(g, device=self.device).reshape(-1).double().sum().item())
 
     # -- writes -----------------------------------------------------------------
     def accumulate(self, msg: GradMessage, *, stream=None) -> None:
@@ -477,7 +475,7 @@ class ParamBuffer(_Paged):
         fidx = buf * self.num_layers + layer
         D.check(N.lib().hm_accumulate(
             D.ptr(src), D.DT_OF_TORCH[src.dtype], D.ptr(self.g16_pool[buf]), self._dt,
-            D.ptr(self._eng.desc.static(ch)), len(ch), 1 if add else 0,
+            D.ptr(self._eng.desc.static(ch)), len(ch), 1 if add else 0, None,
             D.ptr(self._flags) + 4 * fidx, D.ptr(self._sumsq) + 8 * fidx, D.sptr(st)))
         if self._ledger_on:
             self.ledger.record_accumulate(layer, self._pool_sum(buf, layer, st) - old)
@@ -485,6 +483,65 @@ class ParamBuffer(_Paged):
             self.ledger.messages_accumulated[layer] += 1
         self._pending[layer] += 1
         self._max_iter[layer] = max(self._max_iter[layer], msg.iteration)
+
+    def accumulate_flat(self, flat, iteration: int, *, stream=None) -> None:
+        """Accumulate one flat gradient covering every layer in order (the
+        layout a backward pass writes) with ONE K3 launch: the same arithmetic
+        and flags as one ``accumulate`` per layer.  Ledger sums need per-layer
+        reductions, so a ledger-enabled buffer falls back to per-layer calls."""
+        L, lay = self.num_layers, self.layout
+        st = self._stream(stream)
+        with torch.cuda.stream(st):
+            src = D.to_device_flat(flat, self.device)
+        if src.numel() != sum(lay.numels):
+            raise ProtocolError(f"flat gradient has {src.numel()} elements, layers hold "
+                                f"{sum(lay.numels)}")
+        if self._ledger_on:
+            pos = 0
+            for l, n in enumerate(lay.numels):
+                self.accumulate(GradMessage(l, src[pos:pos + n].view(self._shapes[l]), iteration),
+                                stream=st)
+                pos += n
+            return
+        key = tuple(self._gsel)
+        cache = self.__dict__.setdefault("_flat_cache", {})
+        if key not in cache:
+            parts, base = [], 0
+            for l, n in enumerate(lay.numels):
+                c = lay.seg_chunks(l, "16").copy()
+                c["src_off"] += base
+                c["dst_off"] += key[l] * lay.elems16
+                c["slot"] = key[l] * L + l
+                parts.append(c)
+                base += n
+            cache[key] = np.concatenate(parts)
+        chunks = cache[key]
+        modes = np.zeros(2 * L, dtype=np.uint8)
+        reset = []
+        for l in range(L):
+            f = self._gsel[l] * L + l
+            if self._pending[l] > 0:
+                modes[f] = 1
+            else:
+                reset.append(f)
+        with torch.cuda.stream(st):
+            if reset:
+                if reset == list(range(reset[0], reset[0] + len(reset))):
+                    self._flags[reset[0]:reset[0] + len(reset)].zero_()
+                    self._sumsq[reset[0]:reset[0] + len(reset)].zero_()
+                else:
+                    idx = torch.tensor(reset, dtype=torch.int64, device=self.device)
+                    self._flags.index_fill_(0, idx, 0)
+                    self._sumsq.index_fill_(0, idx, 0)
+        dmodes = self._eng.desc.table(modes)
+        D.check(N.lib().hm_accumulate(
+            D.ptr(src), D.DT_OF_TORCH[src.dtype], D.ptr(self.g16_pool), self._dt,
+            D.ptr(self._eng.desc.static(chunks)), len(chunks), 0, D.ptr(dmodes),
+            D.ptr(self._flags), D.ptr(self._sumsq), D.sptr(st)))
+        for l in range(L):
+            self.ledger.messages_accumulated[l] += 1
+            self._pending[l] += 1
+            self._max_iter[l] = max(self._max_iter[l], iteration)
 
     def _hand_over(self, layer: int, stream):
         """Clear-at-take bookkeeping shared by take() and sweep()."""

@@ -1,0 +1,114 @@
+"""torchrun worker for tests/test_gpu_dp.py (one process per GPU, NCCL).
+
+Every rank regenerates every rank's seeded gradients, so each can compute the
+oracle independently: reduced gradient = rn16 sum over ranks (bit-exact at
+N=2, where NCCL performs one bf16 add; within one bf16 ulp of the f32 sum
+otherwise), then the oracle Adam on the CAPTURED post-reduce-scatter pages
+must match the sharded masters bit for bit, and the all-gathered p16 pool
+must equal the cast of the updated masters on every page.
+"""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from oracle import page_adam as O  # noqa: E402
+from paper_2303_02868_b200 import lockfree as LF  # noqa: E402
+from paper_2303_02868_b200.layout import PageLayout  # noqa: E402
+from paper_2303_02868_b200.sharding import ShardedPageStep  # noqa: E402
+
+SIZES = [70001, 1, 5, 32768, 40000, 25003, 777, 65539, 12, 33333, 200000]
+PAGE = 64 * 1024
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    K = int(os.environ.get("DP_BUCKET", "2"))
+    dtype = os.environ.get("DP_DTYPE", "bf16")
+    lay = PageLayout(SIZES, PAGE, world_size=world, rank=rank, bucket_pages=K)
+    rng0 = np.random.default_rng(11)
+    params = [rng0.normal(0, 0.02, n).astype(np.float32) for n in SIZES]
+    dev = torch.device("cuda", local)
+    buf = LF.ParamBuffer([torch.from_numpy(p) for p in params], dtype=dtype, page_bytes=PAGE,
+                         device=dev, layout=lay)
+    ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay)
+    step = ShardedPageStep(buf, ms)
+    om = O.OracleMasters(params)
+    hyper = LF.AdamHyper(lr=1e-3)
+    failures = []
+    for it in range(3):
+        per_rank = []
+        for r in range(world):
+            rr = np.random.default_rng([it, r])
+            gs = []
+            for l, n in enumerate(SIZES):
+                g = rr.normal(0, 1e-2, n).astype(np.float32)
+                if it == 1 and l == 6 and r == world - 1:
+                    g[3] = np.inf   # one rank's non-finite gradient rejects the layer everywhere
+                gs.append(O.to16(g, dtype))
+            per_rank.append(gs)
+        mine = per_rank[rank]
+        flat = np.concatenate(mine)
+        t = torch.from_numpy(flat.view(np.int16) if dtype == "bf16" else flat)
+        if dtype == "bf16":
+            t = t.view(torch.bfloat16)
+        buf.accumulate_flat(t.to(dev), it)
+        gsel = buf._gsel[0]
+        step.step(hyper)
+        # every owner's reduced (post reduce-scatter) pages, gathered so each
+        # rank can run the oracle on the exact captured gradient of ALL pages
+        gathered = buf.g16_pool[gsel].clone()
+        step.coll.all_gather(gathered)
+        torch.cuda.synchronize()
+        gpool = gathered.view(torch.int16).cpu().numpy().view(np.uint16 if dtype == "bf16" else np.float16)
+        for l, n in enumerate(SIZES):
+            red = per_rank[0][l]
+            for r in range(1, world):
+                red = O.accumulate16(red, per_rank[r][l], dtype)
+            captured = red.copy()
+            for s in lay.segments[l]:
+                off = lay.slot16(s.page) * lay.E + s.off
+                got = gpool[off:off + s.n]
+                want = red[s.pos:s.pos + s.n]
+                if world == 2:
+                    if not np.array_equal(got.view(np.uint16), want.view(np.uint16)):
+                        failures.append(f"it{it} layer{l}: reduced grad differs from oracle sum")
+                else:
+                    gf, wf = O.from16(got, dtype), O.from16(want, dtype)
+                    fin = np.isfinite(wf)
+                    if not np.allclose(gf[fin], wf[fin], rtol=2 ** -7, atol=1e-30):
+                        failures.append(f"it{it} layer{l}: reduced grad off by > 1 bf16 ulp")
+                captured[s.pos:s.pos + s.n] = got
+            # oracle Adam on the captured reduced gradient
+            om.update_layer(l, O.from16(captured, dtype), lr=1e-3)
+    steps = ms.steps
+    if steps != om.steps:
+        failures.append(f"steps {steps} != oracle {om.steps}")
+    p16 = buf.p16_pool[buf._psel[0]].view(torch.int16).cpu().numpy().view(np.uint16)
+    for l, n in enumerate(SIZES):
+        mp = ms.p32[l].cpu().numpy() if isinstance(ms.p32[l], torch.Tensor) else ms.p32[l]
+        want16 = O.to16(om.p32[l], dtype).view(np.uint16)
+        for s in lay.segments[l]:
+            off = lay.slot16(s.page) * lay.E + s.off
+            if not np.array_equal(p16[off:off + s.n], want16[s.pos:s.pos + s.n]):
+                failures.append(f"layer{l} page{s.page}: all-gathered p16 differs")
+            if lay.owned(s) and not np.array_equal(mp[s.pos:s.pos + s.n].view(np.uint32),
+                                                   om.p32[l][s.pos:s.pos + s.n].view(np.uint32)):
+                failures.append(f"layer{l} page{s.page}: owned p32 differs")
+    ok = torch.tensor([0 if failures else 1], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if failures:
+        print(f"rank {rank} FAIL:", *failures[:10], sep="\n  ")
+    dist.destroy_process_group()
+    sys.exit(0 if ok.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,27 @@
+"""Data-parallel page step on >= 2 GPUs (torchrun, NCCL): reduce-scatter of
+the gradient pages, flag all-reduce, sharded page-Adam, all-gather of the
+published pages — checked against the oracle in tests/dp_worker.py.
+Skipped on a single-GPU box (run with `gpurun --gpus 2`)."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("bucket,dtype", [(1, "bf16"), (2, "bf16"), (2, "fp16")])
+def test_dp_step_matches_oracle(bucket, dtype):
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if n >= 4 else 2
+    env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29611", str(ROOT / "tests" / "dp_worker.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
