@@ -73,9 +73,25 @@ class PageCollectives:
         mine = whole[lay.rank * blk:(lay.rank + 1) * blk]
         return whole, mine
 
-    def reduce_scatter(self, pool: torch.Tensor, buckets=None, op=dist.ReduceOp.SUM, async_op=False):
+    def reduce_scatter(self, pool: torch.Tensor, buckets=None, op=dist.ReduceOp.SUM, async_op=False,
+                       coalesce: bool | None = None):
+        """In-place RS of each bucket.  With ``coalesce`` (default on NCCL) all
+        buckets go into ONE ncclGroupStart/End, i.e. one fused launch instead
+        of a per-bucket latency each."""
+        buckets = list(range(self.layout.num_buckets) if buckets is None else buckets)
+        if coalesce is None:
+            coalesce = pool.is_cuda and len(buckets) > 1
+        if coalesce:
+            with dist._coalescing_manager(group=self.group, device=pool.device, async_ops=True) as cm:
+                for b in buckets:
+                    whole, mine = self.bucket_views(pool, b)
+                    dist.reduce_scatter_tensor(mine, whole, op=op, group=self.group)
+            if async_op:
+                return [cm]
+            cm.wait()
+            return []
         works = []
-        for b in (range(self.layout.num_buckets) if buckets is None else buckets):
+        for b in buckets:
             whole, mine = self.bucket_views(pool, b)
             works.append(dist.reduce_scatter_tensor(mine, whole, op=op, group=self.group,
                                                     async_op=async_op))
