@@ -350,10 +350,16 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-pages", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c3-layers", type=int, default=8, help="C3 slice (host-memory bound)")
+    ap.add_argument("--swap-group-pages", type=int, default=64)
+    ap.add_argument("--swap-slots", type=int, default=2)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c3":
+        from paper_2303_02868_b200 import swap_bench
+        return swap_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_2303_02868_b200 import dp_bench

@@ -11,15 +11,17 @@
 namespace hm {
 namespace {
 
-__device__ __forceinline__ void flush_stats(bool bad, double sq, uint32_t* nonfinite, double* sumsq,
-                                            uint32_t slot, double* red) {
-  if (nonfinite) {
-    const int any = __syncthreads_or(bad ? 1 : 0);
-    if (any && threadIdx.x == 0) atomicOr(&nonfinite[slot], 1u);
-  }
+// Per-warp flush of the fused statistics: no block barrier, one atomic per
+// warp (the non-finite OR only when a lane saw one).  sumsq feeds the grad
+// norm / clip only, so its f64 atomic order is free to vary.
+__device__ __forceinline__ void flush_stats(bool bad, float sq, uint32_t* nonfinite, double* sumsq,
+                                            uint32_t slot) {
+  const int lane = threadIdx.x & 31;
+  if (nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&nonfinite[slot], 1u);
   if (sumsq) {
-    const double tot = block_sum<kThreads>(sq, red);
-    if (threadIdx.x == 0 && tot != 0.0) atomicAdd(&sumsq[slot], tot);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0 && sq != 0.f) atomicAdd(&sumsq[slot], (double)sq);
   }
 }
 
@@ -31,12 +33,11 @@ __global__ void __launch_bounds__(kThreads)
 accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
                   void* __restrict__ dst, int mode, const uint8_t* __restrict__ slot_modes,
                   uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq) {
-  __shared__ double red[kThreads / 32];
   const hm_seg_chunk c = chunks[blockIdx.x];
   const int add = slot_modes ? (int)slot_modes[c.slot] : mode;
   const int tid = threadIdx.x;
   bool bad = false;
-  double sq = 0.0;
+  float sq = 0.f;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
     F8 a[kVecPerThread], b[kVecPerThread];
@@ -61,7 +62,7 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
       for (int j = 0; j < kVec; ++j) {
         const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b[k].v[j], a[k].v[j])));
         bad |= !is_finite(r);
-        if (sumsq) sq += (double)r * (double)r - (double)b[k].v[j] * (double)b[k].v[j];
+        if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b[k].v[j], b[k].v[j]));
         o.v[j] = r;
       }
       store8<DDT>(dst, c.dst_off + e, o);
@@ -72,11 +73,11 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
       const float b1 = add ? load1<DDT>(dst, c.dst_off + i) : 0.0f;
       const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b1, a1)));
       bad |= !is_finite(r);
-      if (sumsq) sq += (double)r * (double)r - (double)b1 * (double)b1;
+      if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b1, b1));
       store1<DDT>(dst, c.dst_off + i, r);
     }
   }
-  flush_stats(bad, sq, nonfinite, sumsq, c.slot, red);
+  flush_stats(bad, sq, nonfinite, sumsq, c.slot);
 }
 
 template <int SDT, int DDT>
@@ -146,7 +147,7 @@ reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ 
     const double tot = block_sum<kThreads>(s, red);
     if (threadIdx.x == 0) atomicAdd(&sums[c.slot], tot);
   }
-  flush_stats(bad, sq, nonfinite, sumsq, c.slot, red);
+  flush_stats(bad, (float)sq, nonfinite, sumsq, c.slot);
 }
 
 // Byte-run copy: one CTA per descriptor; 16-byte vectors once source and

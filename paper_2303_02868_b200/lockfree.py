@@ -434,12 +434,12 @@ class ParamBuffer(_Paged):
             return self._out(t, layer)
         return self._unpack16(self.g16_pool[self._gsel[layer]], layer)
 
-    def _unpack16(self, pool, layer, readonly=False, stream=None):
+    def _unpack16(self, pool, layer, readonly=False, stream=None, raw=False):
         st = self._stream(stream)
         with torch.cuda.stream(st):
             out = torch.empty(self.layout.numels[layer], dtype=self._t16, device=self.device)
         self._cast(pool, self._dt, out, self._dt, self.layout.seg_chunks(layer, "16", reverse=True), st)
-        return self._out(out, layer, readonly)
+        return out if raw else self._out(out, layer, readonly)
 
     def _pool_sum(self, buf, layer, stream) -> float:
         """f64 sum of the layer's gradient pages — ConservationLedger only
@@ -447,9 +447,9 @@ class ParamBuffer(_Paged):
         unpacked by the page kernel and summed with torch's fixed-order
         reduction so that the same data always yields the same float (the
         ledger compares sums for equality, lockfree.py:311)."""
-        g = self._unpack16(self.g16_pool[buf], layer, stream=stream)
+        g = self._unpack16(self.g16_pool[buf], layer, stream=stream, raw=True)
         with torch.cuda.stream(stream):
-            return float(torch.as_tensor(g, device=self.device).reshape(-1).double().sum().item())
+            return float(g.double().sum().item())
 
     # -- writes -----------------------------------------------------------------
     def accumulate(self, msg: GradMessage, *, stream=None) -> None:

@@ -1,0 +1,190 @@
+"""Page pools with bytes behind them (K1 pack/unpack + K8 page motion).
+
+The reference page manager is metadata-only: ``page_move`` frees at the
+source and claims at the destination, ``tensor_merge`` reassigns ids, and no
+byte ever moves (hiermem/pagemem.py:7-9, 323-326, 386-405).  The paper's
+Allocator/Executor do move them (pre-allocated pools,
+``cudaMemcpyAsync`` between tiers).  ``DevicePageManager`` is the drop-in
+``PageManager`` (same table, same results, same errors) whose GPU pool is an
+HBM byte buffer and whose CPU pool is a pinned host byte buffer:
+
+* ``write(tid, data)`` / ``read(tid)`` pack / unpack a tensor into / out of
+  its pages along the (page, offset, bytes) segments of the table —
+  ``hm_copy_runs`` (16-byte vector copies) on the device, copy engines across
+  the PCIe boundary;
+* ``page_move`` copies the page to its new tier with one cudaMemcpyAsync on
+  a copy stream before returning the reference's TransferDescriptor;
+* ``tensor_merge`` copies every relocated chunk (keeping its in-page offset)
+  through a staging buffer, so chains like page 5 -> 3 while 3 -> 4 are safe.
+
+SSD pools stay metadata-only (no GDS in the image); touching their bytes
+raises ConfigError.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _native as N
+from .errors import ConfigError
+from .pagemem import PageManager, Tier, TransferDescriptor
+
+COPY_PIECE = 64 * 1024  # bytes per CTA work unit of hm_copy_runs
+
+
+def _descs(rows) -> np.ndarray:
+    """Split (src_off, dst_off, bytes) runs into <= COPY_PIECE pieces."""
+    out = []
+    for s, d, n in rows:
+        k = 0
+        while k < n:
+            m = min(COPY_PIECE, n - k)
+            out.append((s + k, d + k, m))
+            k += m
+    return np.array(out, dtype=N.COPY_DESC) if out else np.zeros(0, dtype=N.COPY_DESC)
+
+
+class DevicePageManager(PageManager):
+    def __init__(self, pool_specs, device=None):
+        super().__init__(pool_specs)
+        self.device = D.require_device(device)
+        self.copy_stream = torch.cuda.Stream(self.device)
+        self.storage: dict[Tier, torch.Tensor] = {}
+        for tier, pool in self.pools.items():
+            if tier is Tier.GPU:
+                self.storage[tier] = torch.zeros(pool.capacity_bytes, dtype=torch.uint8, device=self.device)
+            elif tier is Tier.CPU:
+                self.storage[tier] = torch.zeros(pool.capacity_bytes, dtype=torch.uint8, pin_memory=True)
+
+    # -- addressing -----------------------------------------------------------
+    def _loc(self, pid: int):
+        for tier, pool in self.pools.items():
+            if pid in pool.pages:
+                if tier not in self.storage:
+                    raise ConfigError(f"{tier.name} pages have no backing store here (no GDS)")
+                return tier, (pid - pool.first_page_id) * pool.page_bytes
+        raise KeyError(f"unknown page id {pid}")
+
+    def _runs_by_tier(self, tensor_id: int):
+        runs: dict[Tier, list] = {}
+        pos = 0
+        for pid, off, nbytes in self.tensors[tensor_id].segments():
+            tier, base = self._loc(pid)
+            runs.setdefault(tier, []).append((pos, base + off, nbytes))
+            pos += nbytes
+        return runs
+
+    # -- pack / unpack ----------------------------------------------------------
+    def write(self, tensor_id: int, data, *, stream=None) -> None:
+        """Pack a tensor's bytes into its pages (K1)."""
+        t = self.tensors[tensor_id]
+        st = D.cur_stream(self.device, stream)
+        src = data.detach().reshape(-1) if isinstance(data, torch.Tensor) else \
+            torch.from_numpy(np.ascontiguousarray(data).reshape(-1))
+        raw = src.contiguous().view(torch.uint8)
+        if raw.numel() != t.bytes:
+            raise ConfigError(f"tensor {tensor_id} holds {t.bytes} bytes, got {raw.numel()}")
+        lib = N.lib()
+        for tier, rows in self._runs_by_tier(tensor_id).items():
+            store = self.storage[tier]
+            if tier is Tier.GPU:
+                with torch.cuda.stream(st):
+                    dev = raw.to(self.device, non_blocking=raw.is_pinned()) if not raw.is_cuda else raw
+                d = _descs(rows)
+                D.check(lib.hm_copy_runs(D.ptr(dev), D.ptr(store), D.ptr(self._up(d)), len(d), D.sptr(st)))
+                if dev is not raw:
+                    dev.record_stream(st)
+            else:
+                kind = 2 if raw.is_cuda else 0
+                if kind == 0:
+                    st.synchronize()
+                    for s, dpos, n in rows:
+                        store[dpos:dpos + n].copy_(raw[s:s + n].cpu())
+                else:
+                    d = np.array(rows, dtype=N.COPY_DESC)
+                    D.check(lib.hm_memcpy_runs(D.ptr(raw), D.ptr(store), d.ctypes.data, len(d), 2,
+                                               D.sptr(st)))
+
+    def read(self, tensor_id: int, *, stream=None) -> torch.Tensor:
+        """Unpack a tensor's pages into a contiguous CUDA tensor (K1)."""
+        t = self.tensors[tensor_id]
+        st = D.cur_stream(self.device, stream)
+        with torch.cuda.stream(st):
+            out = torch.empty(t.bytes, dtype=torch.uint8, device=self.device)
+        lib = N.lib()
+        for tier, rows in self._runs_by_tier(tensor_id).items():
+            store = self.storage[tier]
+            inv = [(dpos, s, n) for s, dpos, n in rows]
+            if tier is Tier.GPU:
+                d = _descs(inv)
+                D.check(lib.hm_copy_runs(D.ptr(store), D.ptr(out), D.ptr(self._up(d)), len(d), D.sptr(st)))
+            else:
+                d = np.array(inv, dtype=N.COPY_DESC)
+                D.check(lib.hm_memcpy_runs(D.ptr(store), D.ptr(out), d.ctypes.data, len(d), 1, D.sptr(st)))
+        dt = torch.float32 if t.dtype == "fp32" else torch.float16
+        return out.view(dt)
+
+    def _up(self, d: np.ndarray) -> torch.Tensor:
+        return torch.from_numpy(d.view(np.uint8).copy()).to(self.device) if len(d) else \
+            torch.empty(8, dtype=torch.uint8, device=self.device)
+
+    # -- movement with data -----------------------------------------------------------
+    def _tier_of(self, pid: int) -> Tier:
+        for tier, pool in self.pools.items():
+            if pid in pool.pages:
+                return tier
+        raise KeyError(f"unknown page id {pid}")
+
+    def page_move(self, page_id: int, target_tier, *, stream=None) -> TransferDescriptor:
+        backed_src = self._tier_of(page_id) in self.storage
+        src_off = self._loc(page_id)[1] if backed_src else None
+        src_tier = self._tier_of(page_id)
+        desc = super().page_move(page_id, target_tier)
+        if not backed_src or desc.dst_tier not in self.storage:
+            return desc  # an SSD side is metadata-only, as in the reference
+        dst_tier, dst_off = self._loc(desc.new_page_id)
+        st = D.cur_stream(self.device, stream)
+        self.copy_stream.wait_stream(st)
+        kind = {(Tier.GPU, Tier.CPU): 2, (Tier.CPU, Tier.GPU): 1}[(src_tier, dst_tier)]
+        d = np.array([(src_off, dst_off, desc.bytes)], dtype=N.COPY_DESC)
+        D.check(N.lib().hm_memcpy_runs(D.ptr(self.storage[src_tier]), D.ptr(self.storage[dst_tier]),
+                                       d.ctypes.data, 1, kind, D.sptr(self.copy_stream)))
+        st.wait_stream(self.copy_stream)
+        return desc
+
+    def tensor_merge(self, tensor_id: int, *, stream=None) -> dict:
+        t = self.tensors.get(tensor_id)
+        before = t.segments() if t is not None else None
+        report = super().tensor_merge(tensor_id)
+        if report["moved_chunks"] == 0:
+            return report
+        after = self.tensors[tensor_id].segments()
+        moves = []
+        for (p0, o0, n0), (p1, o1, n1) in zip(before, after):
+            if p0 != p1:
+                (t0, a0), (t1, a1) = self._loc(p0), self._loc(p1)
+                if t0 is not t1:
+                    raise ConfigError("merge stays within one tier")
+                moves.append((a0 + o0, a1 + o1, n0))
+        tier = self._loc(after[0][0])[0]
+        store = self.storage[tier]
+        st = D.cur_stream(self.device, stream)
+        total = sum(n for _, _, n in moves)
+        if tier is Tier.GPU:
+            with torch.cuda.stream(st):
+                tmp = torch.empty(total, dtype=torch.uint8, device=self.device)
+            gather, scatter, pos = [], [], 0
+            for a0, a1, n in moves:
+                gather.append((a0, pos, n))
+                scatter.append((pos, a1, n))
+                pos += n
+            g, s = _descs(gather), _descs(scatter)
+            D.check(N.lib().hm_copy_runs(D.ptr(store), D.ptr(tmp), D.ptr(self._up(g)), len(g), D.sptr(st)))
+            D.check(N.lib().hm_copy_runs(D.ptr(tmp), D.ptr(store), D.ptr(self._up(s)), len(s), D.sptr(st)))
+        else:
+            st.synchronize()
+            tmp = [store[a0:a0 + n].clone() for a0, _, n in moves]
+            for (a0, a1, n), buf in zip(moves, tmp):
+                store[a1:a1 + n].copy_(buf)
+        return report

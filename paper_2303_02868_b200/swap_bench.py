@@ -1,0 +1,131 @@
+"""bench.py --config c3: the pinned-host page swap tier (GPT-3 13B page pools,
+fp32 master state in host memory, lock-free update order preserved).
+
+Host memory of the GPU box bounds the slice: the full 13B model needs
+154 GB of pinned fp32 state (12 B/param), so the default run takes the
+first ``--c3-layers`` transformer layers plus the embeddings (every layer
+has the same shape, so params/s is size-independent and the full-model step
+time is the per-param time x 12.85e9, stated in the output).  The roofline
+is PCIe: 12 B/param fetched + 12 B/param stored, against pinned
+cudaMemcpyAsync bandwidth measured on the box in the same run.
+"""
+from __future__ import annotations
+
+import json
+import time
+
+import torch
+
+
+def measure_pcie(device, nbytes=1 << 30, reps=5):
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    s1, s2 = torch.cuda.Stream(device), torch.cuda.Stream(device)
+
+    def timed(fn):
+        best = float("inf")
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            h.copy_(d, non_blocking=True)
+
+    d2 = torch.empty_like(d)
+    h2 = torch.empty_like(h).pin_memory()
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    t_h2d, t_d2h, t_both = timed(h2d), timed(d2h), timed(both)
+    return {"h2d_gbs": nbytes / t_h2d / 1e9, "d2h_gbs": nbytes / t_d2h / 1e9,
+            "bidir_gbs": 2 * nbytes / t_both / 1e9}
+
+
+def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
+    from . import lockfree as LF
+    from . import workloads as W
+    from .layout import PageLayout
+    from .swap import HostMasterState, swap_sweep
+    device = torch.device("cuda", 0)
+    torch.cuda.set_device(device)
+    shape = W.GPTShape(2048, 5120, 20480, args.c3_layers)
+    specs = W.gpt_param16(shape)
+    full_params = W.total_elems(W.config_specs("c3"))
+    page = args.page_mib * 2**20 if args.page_mib else W.config_page_bytes("c3")
+    numels = [s.bytes // 2 for s in specs]
+    layout = PageLayout(numels, page, names=[s.name for s in specs])
+    gen = torch.Generator(device=device)
+    gen.manual_seed(1234)
+    params = [torch.empty(n, dtype=torch.float32, device=device).normal_(0, 0.02, generator=gen)
+              for n in numels]
+    buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout)
+    t0 = time.perf_counter()
+    hm = HostMasterState(params, page_bytes=page, device=device, layout=layout,
+                         group_pages=args.swap_group_pages, slots=args.swap_slots)
+    init_s = time.perf_counter() - t0
+    del params
+    torch.cuda.empty_cache()
+    P = sum(numels)
+    gen.manual_seed(7)
+    tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
+    grads = torch.empty(P, dtype=torch.float32, device=device).normal_(0, 1e-2, generator=gen).to(tdt)
+    hyper = LF.AdamHyper(lr=1e-3)
+    for rnd in range(2):
+        buf.accumulate_flat(grads, rnd)
+        if rnd == 0:
+            swap_sweep(buf, hm, hyper)
+    L = len(specs)
+
+    def rearm():
+        for l in range(L):
+            buf._pending[l] = 1
+
+    for _ in range(args.warmup):
+        rearm()
+        swap_sweep(buf, hm, hyper)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(device)
+    with ClockSampler(0) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(args.steps):
+            rearm()
+            swap_sweep(buf, hm, hyper)
+        b.record(stream)
+        torch.cuda.synchronize()
+    ms_step = a.elapsed_time(b) / args.steps
+    pcie = measure_pcie(device)
+    moved = 24 * P  # 12 B fetched + 12 B stored per param
+    achieved = moved / (ms_step / 1e3) / 1e9
+    line = {
+        "metric": metric, "value": P / (ms_step / 1e3), "unit": "params/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"c3: GPT-3 13B page pools, first {args.c3_layers} of 40 layers + "
+                               "embeddings; fp32 state in pinned host memory (swap tier)",
+                   "params": P, "full_model_params": full_params, "layers": L, "page_bytes": page,
+                   "pages": layout.used_pages, "group_pages": args.swap_group_pages,
+                   "staging_slots": args.swap_slots, "host_state_gb": 12 * P / 1e9,
+                   "host_init_s": init_s,
+                   "full_model_step_ms_extrapolated": ms_step * full_params / P},
+        "roofline": {"bound": "pcie", "achieved": achieved, "peak": pcie["bidir_gbs"], "unit": "GB/s",
+                     "frac": achieved / pcie["bidir_gbs"], "peak_kind": "measured pinned cudaMemcpyAsync "
+                     "H2D||D2H on this box", "bytes_per_param": 24, "pcie": pcie},
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps * (1 + hm.num_groups),
+    }
+    print(json.dumps(line), flush=True)
