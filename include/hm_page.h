@@ -187,6 +187,34 @@ int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_l
                  float* p32, float* m32, float* v32, void* p16, int p16_dtype,
                  const hm_adam_hyper* hyper, void* stream);
 
+/* ---- data-parallel page collectives fused with compute (NVLink/NVSwitch) ---
+ * Pools are symmetric buffers mapped into every rank (peer virtual addresses,
+ * optionally one NVLS multicast address).  Ownership: page % N
+ * (hiermem/scheduler.py:72-76); the reference models these transfers only
+ * (hiermem/simengine.py:255-257) and has no reduce-scatter.
+ * peer arrays are HOST arrays of n_peers (<= 8) device addresses in rank order. */
+typedef struct hm_seg_chunk hm_seg_chunk;
+
+/* Gradient reduce-scatter of the owned pages fused with the layer's finite
+ * flag and squared norm: local[off] = rn16(sum_r peer_r[off]) in f32, rank
+ * order 0..N-1 (P2P loads), or the switch's sum (mc_pool != NULL: NVLS
+ * multimem.ld_reduce).  chunks: owned pool segments, slot = layer. */
+int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_pool,
+                       void* local_pool, int dtype, const hm_seg_chunk* chunks, int64_t n_chunks,
+                       uint32_t* nonfinite, double* sumsq, void* stream);
+/* flags_out[l] = OR_r peer_flags_r[l]; sumsq_out[l] = sum_r peer_sumsq_r[l]
+ * (rank order).  Replaces an all-reduce of the per-layer reject flags. */
+int hm_dp_flags_merge(const uint64_t* peer_flags, const uint64_t* peer_sumsq, int n_peers,
+                      int n_layers, uint32_t* flags_out, double* sumsq_out, void* stream);
+/* hm_adam_main whose publish epilogue writes each 16-bit page into every
+ * peer's p16 pool (P2P stores) or once through the NVLS multicast address
+ * (mc_p16 != NULL): the parameter all-gather fused into the update. */
+int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* groups,
+                    const hm_group_rt* rt, const void* g, int g_dtype,
+                    float* p32, float* m32, float* v32,
+                    const uint64_t* peer_p16, int n_peers, void* mc_p16, int p16_dtype,
+                    const hm_adam_hyper* hyper, void* stream);
+
 /* Elementwise segment chunk used by accumulate / cast / reduce. */
 typedef struct hm_seg_chunk {
   uint64_t src_off;   /* element offset into src */

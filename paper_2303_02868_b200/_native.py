@@ -77,6 +77,10 @@ SIGNATURES = {
                                 _P, _INT, _P]),
     "hm_adam_main": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT,
                             C.POINTER(AdamHyperC), _P]),
+    "hm_dp_reduce_check": (_INT, [_P, _INT, _P, _P, _INT, _P, _I64, _P, _P, _P]),
+    "hm_dp_flags_merge": (_INT, [_P, _P, _INT, _INT, _P, _P, _P]),
+    "hm_adam_main_ag": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT, _P, _INT,
+                               C.POINTER(AdamHyperC), _P]),
     "hm_accumulate": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P]),
     "hm_cast": (_INT, [_P, _INT, _P, _INT, _P, _I64, _P]),
     "hm_reduce_stats": (_INT, [_P, _INT, _P, _I64, _P, _P, _P, _P]),

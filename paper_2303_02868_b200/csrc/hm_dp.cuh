@@ -1,0 +1,17 @@
+// Peer-pointer plumbing shared by the fused data-parallel kernels.
+#pragma once
+#include <stdint.h>
+
+namespace hm {
+
+constexpr int kMaxPeers = 8;  // one NVLink/NVSwitch domain of a B200 box
+
+// Passed by value as a kernel parameter: no device-side pointer table.
+struct PeerPtrs {
+  uint64_t p[kMaxPeers];
+  int n;
+};
+
+int make_peers(const uint64_t* ptrs, int n, PeerPtrs* out);
+
+}  // namespace hm

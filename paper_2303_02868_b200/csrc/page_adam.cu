@@ -17,6 +17,7 @@
 // decided once per layer by the prologue from the flag that the gradient's
 // producer (hm_accumulate / hm_reduce_stats) fused into its own pass.
 #include "hm_device.cuh"
+#include "hm_dp.cuh"
 #include "hm_error.h"
 
 namespace hm {
@@ -93,12 +94,49 @@ __device__ __forceinline__ void adam_elem(const AdamScalars& s, float g, float& 
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(s.lr, mh), den));
 }
 
-template <int GDT, int PDT>
+// Publish modes of the 16-bit epilogue: local pool, every peer's pool (P2P
+// stores over NVLink = a fused all-gather), or one NVLS multicast store.
+constexpr int kPubLocal = 0, kPubPeers = 1, kPubMulticast = 2;
+
+template <int PDT, int PUB>
+__device__ __forceinline__ void publish8(void* p16, const PeerPtrs& peers, char* mc, uint64_t po,
+                                         const F8& v) {
+  if constexpr (PUB == kPubLocal) {
+    store8<PDT>(p16, po, v);
+  } else {
+    using T = typename Elem<PDT>::T;
+    uint4 u;
+    T* h = reinterpret_cast<T*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = Elem<PDT>::narrow(v.v[i]);
+    if constexpr (PUB == kPubPeers) {
+#pragma unroll
+      for (int r = 0; r < kMaxPeers; ++r)
+        if (r < peers.n) st_stream_u4(reinterpret_cast<T*>(peers.p[r]) + po, u);
+    } else {
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(
+                       mc + po * sizeof(T)),
+                   "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+                   : "memory");
+    }
+  }
+}
+
+template <int PDT, int PUB>
+__device__ __forceinline__ void publish1(void* p16, const PeerPtrs& peers, uint64_t po, float x) {
+  if constexpr (PUB == kPubLocal) {
+    store1<PDT>(p16, po, x);
+  } else {
+    for (int r = 0; r < peers.n; ++r) store1<PDT>(reinterpret_cast<void*>(peers.p[r]), po, x);
+  }
+}
+
+template <int GDT, int PDT, int PUB = kPubLocal>
 __global__ void __launch_bounds__(kThreads)
 adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ groups,
           const hm_group_rt* __restrict__ rt, const void* __restrict__ g,
           float* __restrict__ p32, float* __restrict__ m32, float* __restrict__ v32,
-          void* __restrict__ p16, hm_adam_hyper hyper) {
+          void* __restrict__ p16, hm_adam_hyper hyper, PeerPtrs peers, char* mc) {
   const hm_adam_chunk c = chunks[blockIdx.x];
   const hm_group_launch gl = groups[c.slot];
   const hm_group_rt r = rt[c.slot];
@@ -112,7 +150,7 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
   if (!r.apply) {
     // Rejected layer: state untouched; still publish the unchanged masters.
     if constexpr (kPub) {
-      for (uint32_t i = tid; i < n; i += kThreads) store1<PDT>(p16, po + i, p32[so + i]);
+      for (uint32_t i = tid; i < n; i += kThreads) publish1<PDT, PUB>(p16, peers, po + i, p32[so + i]);
     }
     return;
   }
@@ -153,7 +191,7 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
       store8<HM_DT_F32>(p32, so + e, pv[k]);
       store8<HM_DT_F32>(m32, so + e, mv[k]);
       store8<HM_DT_F32>(v32, so + e, vv[k]);
-      if constexpr (kPub) store8<PDT>(p16, po + e, pv[k]);
+      if constexpr (kPub) publish8<PDT, PUB>(p16, peers, mc, po + e, pv[k]);
     }
   } else {
     for (uint32_t i = tid; i < n; i += kThreads) {
@@ -163,13 +201,23 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
       p32[so + i] = p;
       m32[so + i] = m;
       v32[so + i] = v;
-      if constexpr (kPub) store1<PDT>(p16, po + i, p);
+      if constexpr (kPub) publish1<PDT, PUB>(p16, peers, po + i, p);
     }
   }
 }
 
 using AdamFn = void (*)(const hm_adam_chunk*, const hm_group_launch*, const hm_group_rt*,
-                        const void*, float*, float*, float*, void*, hm_adam_hyper);
+                        const void*, float*, float*, float*, void*, hm_adam_hyper, PeerPtrs, char*);
+
+AdamFn pick_adam_ag(int gdt, int pdt, int pub) {
+  if (gdt != HM_DT_BF16 && gdt != HM_DT_F16) return nullptr;
+  if (pdt != gdt) return nullptr;
+  if (gdt == HM_DT_BF16)
+    return pub == kPubPeers ? adam_main<HM_DT_BF16, HM_DT_BF16, kPubPeers>
+                            : adam_main<HM_DT_BF16, HM_DT_BF16, kPubMulticast>;
+  return pub == kPubPeers ? adam_main<HM_DT_F16, HM_DT_F16, kPubPeers>
+                          : adam_main<HM_DT_F16, HM_DT_F16, kPubMulticast>;
+}
 
 template <int GDT>
 AdamFn pick_p(int pdt) {
@@ -232,8 +280,29 @@ extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
   hm::AdamFn fn = hm::pick_adam(g_dtype, pdt);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (n_chunks == 0) return HM_OK;
+  hm::PeerPtrs none{};
   fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      chunks, groups, rt, g, p32, m32, v32, p16, *hyper);
+      chunks, groups, rt, g, p32, m32, v32, p16, *hyper, none, nullptr);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+extern "C" int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks,
+                               const hm_group_launch* groups, const hm_group_rt* rt, const void* g,
+                               int g_dtype, float* p32, float* m32, float* v32,
+                               const uint64_t* peer_p16, int n_peers, void* mc_p16, int p16_dtype,
+                               const hm_adam_hyper* hyper, void* stream) {
+  if (!hyper || !rt) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: missing hyper/rt");
+  hm::PeerPtrs peers;
+  if (int rc = hm::make_peers(peer_p16, n_peers, &peers)) return rc;
+  const int pub = mc_p16 ? hm::kPubMulticast : hm::kPubPeers;
+  hm::AdamFn fn = hm::pick_adam_ag(g_dtype, p16_dtype, pub);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: unsupported dtypes g=%d p16=%d", g_dtype, p16_dtype);
+  if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: bad chunk count");
+  if (n_chunks == 0) return HM_OK;
+  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      chunks, groups, rt, g, p32, m32, v32, nullptr, *hyper, peers, static_cast<char*>(mc_p16));
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }

@@ -1,0 +1,216 @@
+// Data-parallel page collectives fused with their compute, over NVLink /
+// NVSwitch peer memory (symmetric buffers mapped into every rank).
+//
+//   hm_dp_reduce_check   gradient reduce-scatter of the owned pages fused with
+//                        the layer's finite flag and squared norm (K6 + K3):
+//                        each owner reads its pages from every peer (P2P
+//                        loads, summed in f32 in rank order 0..N-1 and rounded
+//                        once — deterministic), or asks the switch for the sum
+//                        (NVLS multimem.ld_reduce, inbound S/N bytes per rank).
+//   hm_dp_flags_merge    OR of the per-layer flags / sum of the norms over
+//                        peers (replaces an all-reduce of a few hundred words).
+//   hm_adam_main_ag      (page_adam.cu) page-Adam whose publish epilogue writes
+//                        the 16-bit pages into every peer's pool (P2P stores or
+//                        one NVLS multimem.st): the all-gather (K7) fused into
+//                        the update, tile by tile.
+//
+// The reference only models these transfers (hiermem/simengine.py:255-257,
+// all_gather = lat + page*(N-1)/N / bw) and has no reduce-scatter
+// (SPEC.md:348); ownership is hiermem/scheduler.py:72-76 (page % N).
+#include "hm_device.cuh"
+#include "hm_dp.cuh"
+#include "hm_error.h"
+
+namespace hm {
+namespace {
+
+__device__ __forceinline__ uint4 ld_peer_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <int DT>
+__device__ __forceinline__ uint4 ld_reduce_mc(const void* p);
+
+template <>
+__device__ __forceinline__ uint4 ld_reduce_mc<HM_DT_BF16>(const void* p) {
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+template <>
+__device__ __forceinline__ uint4 ld_reduce_mc<HM_DT_F16>(const void* p) {
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void flush(bool bad, float sq, uint32_t* nonfinite, double* sumsq,
+                                      uint32_t slot) {
+  __shared__ float s_sq[kThreads / 32];
+  __shared__ int s_bad[kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const int any = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    s_sq[warp] = sq;
+    s_bad[warp] = any;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    int b = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      t += s_sq[w];
+      b |= s_bad[w];
+    }
+    if (nonfinite && b) atomicOr(&nonfinite[slot], 1u);
+    if (sumsq && t != 0.f) atomicAdd(&sumsq[slot], (double)t);
+  }
+}
+
+// One CTA per owned chunk; chunk offsets are pool element offsets.
+template <int DT, bool MC>
+__global__ void __launch_bounds__(kThreads)
+reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, PeerPtrs peers, const char* mc,
+                    void* __restrict__ local, uint32_t* __restrict__ nonfinite,
+                    double* __restrict__ sumsq) {
+  using T = typename Elem<DT>::T;
+  const hm_seg_chunk c = chunks[blockIdx.x];
+  const uint64_t off = c.src_off;
+  const int tid = threadIdx.x;
+  bool bad = false;
+  float sq = 0.f;
+  const bool vec = ((off | (uint64_t)c.n) & (kVec - 1)) == 0;
+  if (vec) {
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e >= c.n) continue;
+      F8 acc;
+      if constexpr (MC) {
+        uint4 u = ld_reduce_mc<DT>(mc + (off + e) * sizeof(T));
+        const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) acc.v[j] = Elem<DT>::widen(h[j]);
+      } else {
+        uint4 u[kMaxPeers];
+#pragma unroll
+        for (int r = 0; r < kMaxPeers; ++r)
+          if (r < peers.n) u[r] = ld_peer_u4(reinterpret_cast<const T*>(peers.p[r]) + off + e);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) acc.v[j] = 0.f;
+#pragma unroll
+        for (int r = 0; r < kMaxPeers; ++r) {
+          if (r >= peers.n) break;
+          const T* h = reinterpret_cast<const T*>(&u[r]);
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) acc.v[j] = __fadd_rn(acc.v[j], Elem<DT>::widen(h[j]));
+        }
+      }
+      F8 o;
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const float r = Elem<DT>::widen(Elem<DT>::narrow(acc.v[j]));
+        bad |= !is_finite(r);
+        sq += __fmul_rn(r, r);
+        o.v[j] = r;
+      }
+      store8<DT>(local, off + e, o);
+    }
+  } else {
+    for (uint32_t i = tid; i < c.n; i += kThreads) {
+      float a = 0.f;
+      for (int r = 0; r < peers.n; ++r)
+        a = __fadd_rn(a, Elem<DT>::widen(reinterpret_cast<const T*>(peers.p[r])[off + i]));
+      const float r = Elem<DT>::widen(Elem<DT>::narrow(a));
+      bad |= !is_finite(r);
+      sq += __fmul_rn(r, r);
+      store1<DT>(local, off + i, r);
+    }
+  }
+  flush(bad, sq, nonfinite, sumsq, c.slot);
+}
+
+__global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, int n,
+                                   uint32_t* __restrict__ flags_out, double* __restrict__ sumsq_out) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
+    uint32_t f = 0;
+    double s = 0.0;
+    for (int r = 0; r < flag_peers.n; ++r) {
+      f |= reinterpret_cast<const volatile uint32_t*>(flag_peers.p[r])[l];
+      if (sumsq_out) s += reinterpret_cast<const volatile double*>(sumsq_peers.p[r])[l];
+    }
+    flags_out[l] = f;
+    if (sumsq_out) sumsq_out[l] = s;
+  }
+}
+
+using RcFn = void (*)(const hm_seg_chunk*, PeerPtrs, const char*, void*, uint32_t*, double*);
+
+RcFn pick_rc(int dt, bool mc) {
+  if (dt == HM_DT_BF16) return mc ? reduce_check_kernel<HM_DT_BF16, true> : reduce_check_kernel<HM_DT_BF16, false>;
+  if (dt == HM_DT_F16) return mc ? reduce_check_kernel<HM_DT_F16, true> : reduce_check_kernel<HM_DT_F16, false>;
+  return nullptr;
+}
+
+}  // namespace
+
+int make_peers(const uint64_t* ptrs, int n, PeerPtrs* out) {
+  if (n < 1 || n > kMaxPeers || !ptrs)
+    return hm_set_error(HM_ERR_INVALID, "peer count %d outside 1..%d", n, kMaxPeers);
+  out->n = n;
+  for (int i = 0; i < kMaxPeers; ++i) out->p[i] = i < n ? ptrs[i] : 0;
+  return HM_OK;
+}
+
+}  // namespace hm
+
+extern "C" {
+
+int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_pool,
+                       void* local_pool, int dtype, const hm_seg_chunk* chunks, int64_t n_chunks,
+                       uint32_t* nonfinite, double* sumsq, void* stream) {
+  hm::PeerPtrs peers;
+  if (int rc = hm::make_peers(peer_pools, n_peers, &peers)) return rc;
+  hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
+  if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
+    return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: bad chunk count");
+  if (n_chunks == 0) return HM_OK;
+  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      chunks, peers, static_cast<const char*>(mc_pool), local_pool, nonfinite, sumsq);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_dp_flags_merge(const uint64_t* peer_flags, const uint64_t* peer_sumsq, int n_peers,
+                      int n_layers, uint32_t* flags_out, double* sumsq_out, void* stream) {
+  hm::PeerPtrs f, s;
+  if (int rc = hm::make_peers(peer_flags, n_peers, &f)) return rc;
+  if (peer_sumsq) {
+    if (int rc = hm::make_peers(peer_sumsq, n_peers, &s)) return rc;
+  } else {
+    s = f;
+    sumsq_out = nullptr;
+  }
+  if (n_layers <= 0) return HM_OK;
+  const int blocks = (n_layers + 255) / 256;
+  hm::flags_merge_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(f, s, n_layers,
+                                                                                flags_out, sumsq_out);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+}  // extern "C"

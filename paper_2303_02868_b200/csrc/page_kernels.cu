@@ -11,17 +11,33 @@
 namespace hm {
 namespace {
 
-// Per-warp flush of the fused statistics: no block barrier, one atomic per
-// warp (the non-finite OR only when a lane saw one).  sumsq feeds the grad
-// norm / clip only, so its f64 atomic order is free to vary.
+// Flush of the fused statistics: warp shuffles, ONE block barrier, then one
+// atomic per CTA (per-warp f64 atomics on a few hundred layer addresses
+// serialise in L2 and cost 3x in measurement).  sumsq feeds the grad norm /
+// clip only, so its f64 atomic order is free to vary.
 __device__ __forceinline__ void flush_stats(bool bad, float sq, uint32_t* nonfinite, double* sumsq,
                                             uint32_t slot) {
-  const int lane = threadIdx.x & 31;
-  if (nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&nonfinite[slot], 1u);
-  if (sumsq) {
+  __shared__ float s_sq[kThreads / 32];
+  __shared__ int s_bad[kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if (lane == 0 && sq != 0.f) atomicAdd(&sumsq[slot], (double)sq);
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const int any = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    s_sq[warp] = sq;
+    s_bad[warp] = any;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    int b = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      t += s_sq[w];
+      b |= s_bad[w];
+    }
+    if (nonfinite && b) atomicOr(&nonfinite[slot], 1u);
+    if (sumsq && t != 0.f) atomicAdd(&sumsq[slot], (double)t);
   }
 }
 

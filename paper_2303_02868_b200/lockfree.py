@@ -376,7 +376,7 @@ class ParamBuffer(_Paged):
 
     def __init__(self, initial_params, *, dtype: str = "fp16", page_bytes: int = PAGE_BYTES_DEFAULT,
                  device=None, layout: PageLayout | None = None, ledger: bool = False,
-                 world_size: int = 1, rank: int = 0):
+                 world_size: int = 1, rank: int = 0, pool_alloc=None):
         if dtype not in D.TORCH16:
             raise ConfigError(f"dtype must be one of {sorted(D.TORCH16)}, got {dtype!r}")
         self._init_paged(initial_params, page_bytes, device, layout, world_size, rank)
@@ -386,8 +386,14 @@ class ParamBuffer(_Paged):
         L, lay = self.num_layers, self.layout
         st = self._stream()
         with torch.cuda.stream(st):
-            self.g16_pool = torch.zeros(2, lay.elems16, dtype=self._t16, device=self.device)
-            self.p16_pool = torch.zeros(2, lay.elems16, dtype=self._t16, device=self.device)
+            if pool_alloc is None:
+                self.g16_pool = torch.zeros(2, lay.elems16, dtype=self._t16, device=self.device)
+                self.p16_pool = torch.zeros(2, lay.elems16, dtype=self._t16, device=self.device)
+            else:  # e.g. sharding.symmetric_alloc: peer-mapped pools for the fused DP step
+                self.g16_pool = pool_alloc((2, lay.elems16), self._t16, self.device)
+                self.p16_pool = pool_alloc((2, lay.elems16), self._t16, self.device)
+                self.g16_pool.zero_()
+                self.p16_pool.zero_()
             self._flags = torch.zeros(2 * L, dtype=torch.int32, device=self.device)
             self._sumsq = torch.zeros(2 * L, dtype=torch.float64, device=self.device)
         self._gsel = [0] * L

@@ -207,3 +207,138 @@ class ShardedPageStep:
         if timings is not None:
             timings["_marks"] = marks
         return list(range(L))
+
+
+# ---- fused path over symmetric (peer-mapped) page pools ------------------------------
+
+def symmetric_alloc(shape, dtype, device):
+    """Allocator for ParamBuffer pools that every rank can map (torch symmetric
+    memory: cuMem handles exchanged at rendezvous, optional NVLS multicast)."""
+    import torch.distributed._symmetric_memory as symm
+    return symm.empty(*shape, dtype=dtype, device=device)
+
+
+class FusedShardedPageStep:
+    """The DP page step with the collectives fused into the page kernels:
+
+        barrier -> hm_dp_reduce_check (owned pages read from every peer's
+        gradient pool, f32 sum in rank order, rounded once; flags + norm)
+        -> barrier -> hm_dp_flags_merge -> prologue ->
+        hm_adam_main_ag (update + publish into every peer's p16 pool)
+        -> barrier
+
+    ``mode="p2p"`` moves the bytes with NVLink peer loads/stores;
+    ``mode="nvls"`` uses the NVSwitch multicast address: the reduction
+    happens in the switch (multimem.ld_reduce) and one store reaches every
+    GPU (multimem.st).  The buffer's pools must come from ``symmetric_alloc``.
+    """
+
+    def __init__(self, buffer, masters, group=None, mode: str = "p2p"):
+        import torch.distributed._symmetric_memory as symm
+        lay = buffer.layout
+        if masters.layout.numels != lay.numels or masters.layout.world_size != lay.world_size:
+            raise ConfigError("buffer and masters must share the sharded page layout")
+        if mode not in ("p2p", "nvls"):
+            raise ConfigError(f"unknown fused DP mode {mode!r}")
+        self.buffer, self.masters, self.layout = buffer, masters, lay
+        self.group = group if group is not None else dist.group.WORLD
+        gname = self.group.group_name
+        self.device = buffer.device
+        L = buffer.num_layers
+        self.h_g = symm.rendezvous(buffer.g16_pool, gname)
+        self.h_p = symm.rendezvous(buffer.p16_pool, gname)
+        self.flags_local = symm.empty(L, dtype=torch.int32, device=self.device)
+        self.sumsq_local = symm.empty(L, dtype=torch.float64, device=self.device)
+        self.h_f = symm.rendezvous(self.flags_local, gname)
+        self.h_s = symm.rendezvous(self.sumsq_local, gname)
+        self.flags = torch.zeros(L, dtype=torch.int32, device=self.device)
+        self.sumsq = torch.zeros(L, dtype=torch.float64, device=self.device)
+        self.n = lay.world_size
+        mc_g = int(getattr(self.h_g, "multicast_ptr", 0) or 0)
+        mc_p = int(getattr(self.h_p, "multicast_ptr", 0) or 0)
+        if mode == "nvls" and (not mc_g or not mc_p):
+            raise ConfigError("NVLS multicast is not available on this system (multicast_ptr is 0)")
+        self.mode = mode
+        self.mc_g, self.mc_p = (mc_g, mc_p) if mode == "nvls" else (0, 0)
+        self.g_ptrs = [int(p) for p in self.h_g.buffer_ptrs]
+        self.p_ptrs = [int(p) for p in self.h_p.buffer_ptrs]
+        self.f_ptrs = [int(p) for p in self.h_f.buffer_ptrs]
+        self.s_ptrs = [int(p) for p in self.h_s.buffer_ptrs]
+        self._check_chunks = lay.pool_chunks(range(L), "16", owned_only=True)
+        self._adam_chunks = lay.adam_chunks(range(L), "pool", owned_only=True)
+
+    @staticmethod
+    def _arr(ptrs):
+        import ctypes as C
+        return (C.c_uint64 * len(ptrs))(*ptrs)
+
+    def step(self, hyper, *, stream=None, timings: dict | None = None):
+        buf, ms, lay = self.buffer, self.masters, self.layout
+        st = buf._stream(stream)
+        L = buf.num_layers
+        if any(p == 0 for p in buf._pending):
+            raise ConfigError("a DP page step needs a gradient for every layer on every rank")
+        gsel, psel = buf._gsel[0], buf._psel[0]
+        if any(x != gsel for x in buf._gsel) or any(x != psel for x in buf._psel):
+            raise ConfigError("DP page step expects all layers in the same page buffers")
+        span_b = lay.elems16 * buf.g16_pool.element_size()
+        marks = {}
+
+        def mark(name):
+            if timings is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                marks[name] = e
+
+        lib, eng = N.lib(), ms._eng
+        with torch.cuda.stream(st):
+            mark("start")
+            self.flags_local.zero_()
+            if getattr(hyper, "max_norm", 0.0) > 0:
+                self.sumsq_local.zero_()
+            self.h_g.barrier(channel=0)                          # every rank's gradients are complete
+            gp = self._arr([p + gsel * span_b for p in self.g_ptrs])
+            mc = self.mc_g + gsel * span_b if self.mc_g else None
+            ch = self._check_chunks
+            D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
+                                           D.ptr(eng.desc.static(ch)), len(ch), D.ptr(self.flags_local),
+                                           D.ptr(self.sumsq_local), D.sptr(st)))
+            mark("rs")
+            self.h_f.barrier(channel=0)                          # flags / norms visible to all
+            clip = getattr(hyper, "max_norm", 0.0) > 0
+            D.check(lib.hm_dp_flags_merge(self._arr(self.f_ptrs), self._arr(self.s_ptrs) if clip else None,
+                                          self.n, L, D.ptr(self.flags), D.ptr(self.sumsq) if clip else None,
+                                          D.sptr(st)))
+            mark("check")
+        counts, newest = [], []
+        for l in range(L):
+            _, c, nw = buf._hand_over(l, st)
+            counts.append(c)
+            newest.append(nw)
+        span = lay.elems16
+        groups = np.zeros(L, dtype=N.GROUP_LAUNCH)
+        for l in range(L):
+            groups[l] = (gsel * span, (psel ^ 1) * span, l, l)
+        dgroups = eng.desc.table(groups)
+        rt = eng.rt_scratch(L)
+        bc, bc_len = ms._bias(hyper, range(L))
+        hc = D.hyper_c(hyper)
+        D.check(lib.hm_adam_prologue(D.ptr(dgroups), L, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
+                                     D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(self.flags),
+                                     D.ptr(self.sumsq), 1, D.sptr(st)))
+        ac = self._adam_chunks
+        D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(ac)), len(ac), D.ptr(dgroups), D.ptr(rt),
+                                    D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool), D.ptr(ms.m32_pool),
+                                    D.ptr(ms.v32_pool), self._arr(self.p_ptrs), self.n,
+                                    self.mc_p if self.mc_p else None, buf._dt, hc, D.sptr(st)))
+        with torch.cuda.stream(st):
+            mark("adam")
+            self.h_p.barrier(channel=0)                          # published pages landed everywhere
+            mark("ag")
+        for l in range(L):
+            buf._psel[l] ^= 1
+            buf._version[l] += 1
+            buf._applied_iter[l] = newest[l]
+        if timings is not None:
+            timings["_marks"] = marks
+        return list(range(L))

@@ -19,7 +19,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from oracle import page_adam as O  # noqa: E402
 from paper_2303_02868_b200 import lockfree as LF  # noqa: E402
 from paper_2303_02868_b200.layout import PageLayout  # noqa: E402
-from paper_2303_02868_b200.sharding import ShardedPageStep  # noqa: E402
+from paper_2303_02868_b200.sharding import (FusedShardedPageStep, ShardedPageStep,  # noqa: E402
+                                            symmetric_alloc)
 
 SIZES = [70001, 1, 5, 32768, 40000, 25003, 777, 65539, 12, 33333, 200000]
 PAGE = 64 * 1024
@@ -36,13 +37,20 @@ def main():
     rng0 = np.random.default_rng(11)
     params = [rng0.normal(0, 0.02, n).astype(np.float32) for n in SIZES]
     dev = torch.device("cuda", local)
+    mode = os.environ.get("DP_MODE", "nccl")
     buf = LF.ParamBuffer([torch.from_numpy(p) for p in params], dtype=dtype, page_bytes=PAGE,
-                         device=dev, layout=lay)
+                         device=dev, layout=lay, pool_alloc=None if mode == "nccl" else symmetric_alloc)
     ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay)
-    step = ShardedPageStep(buf, ms)
+    step = ShardedPageStep(buf, ms) if mode == "nccl" else FusedShardedPageStep(buf, ms, mode=mode)
+    if mode == "nvls" and step is None:
+        sys.exit(0)
+    from paper_2303_02868_b200.sharding import PageCollectives
+    coll = PageCollectives(lay)
     om = O.OracleMasters(params)
     hyper = LF.AdamHyper(lr=1e-3)
     failures = []
+    if mode != "nccl":
+        print(f"rank {rank}: fused mode {mode}, mc={getattr(step, 'mc_g', 0)}", flush=True)
     for it in range(3):
         per_rank = []
         for r in range(world):
@@ -65,19 +73,25 @@ def main():
         # every owner's reduced (post reduce-scatter) pages, gathered so each
         # rank can run the oracle on the exact captured gradient of ALL pages
         gathered = buf.g16_pool[gsel].clone()
-        step.coll.all_gather(gathered)
+        coll.all_gather(gathered)
         torch.cuda.synchronize()
         gpool = gathered.view(torch.int16).cpu().numpy().view(np.uint16 if dtype == "bf16" else np.float16)
         for l, n in enumerate(SIZES):
-            red = per_rank[0][l]
-            for r in range(1, world):
-                red = O.accumulate16(red, per_rank[r][l], dtype)
+            if mode == "nccl":   # NCCL ring: each hop adds into a 16-bit buffer
+                red = per_rank[0][l]
+                for r in range(1, world):
+                    red = O.accumulate16(red, per_rank[r][l], dtype)
+            else:                # fused kernel: f32 sum in rank order, rounded once
+                acc = O.from16(per_rank[0][l], dtype).copy()
+                for r in range(1, world):
+                    acc = np.add(acc, O.from16(per_rank[r][l], dtype))
+                red = O.to16(acc, dtype)
             captured = red.copy()
             for s in lay.segments[l]:
                 off = lay.slot16(s.page) * lay.E + s.off
                 got = gpool[off:off + s.n]
                 want = red[s.pos:s.pos + s.n]
-                if world == 2:
+                if world == 2 or mode == "p2p":
                     if not np.array_equal(got.view(np.uint16), want.view(np.uint16)):
                         failures.append(f"it{it} layer{l}: reduced grad differs from oracle sum")
                 else:

@@ -18,7 +18,8 @@ t.fill_(r + 1)
 h = symm.rendezvous(t, dist.group.WORLD.group_name)
 mc = getattr(h, "multicast_ptr", None)
 print(r, "ptrs", [hex(p) for p in h.buffer_ptrs], "mc", hex(mc) if mc else mc,
-      "has_mc", h.has_multicast_support() if hasattr(h, "has_multicast_support") else None,
+      "has_mc", symm._SymmetricMemory.has_multicast_support(torch._C._autograd.DeviceType.CUDA, local)
+      if hasattr(torch._C, "_autograd") else None,
       "signal_pad", h.signal_pad_size, flush=True)
 h.barrier()
 peer = h.get_buffer((r + 1) % w, (1 << 20,), torch.bfloat16)
