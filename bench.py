@@ -171,7 +171,7 @@ def run_reference(args):
 
 # ---- the GPU arm ----------------------------------------------------------------------
 
-def build_state(args, device, world=1, rank=0):
+def build_state(args, device, world=1, rank=0, pool_alloc=None):
     import torch
     from paper_2303_02868_b200 import lockfree as LF
     from paper_2303_02868_b200 import workloads as W
@@ -186,7 +186,8 @@ def build_state(args, device, world=1, rank=0):
     gen.manual_seed(1234)
     params = [torch.empty(n, dtype=torch.float32, device=device).normal_(0, 0.02, generator=gen)
               for n in numels]
-    buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout)
+    buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout,
+                         pool_alloc=pool_alloc)
     ms = LF.MasterState(params, page_bytes=page, device=device, layout=layout)
     del params
     torch.cuda.empty_cache()
@@ -345,7 +346,10 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
     ap.add_argument("--page-mib", type=int, default=0)
-    ap.add_argument("--bucket-pages", type=int, default=8)
+    ap.add_argument("--bucket-pages", type=int, default=32)
+    ap.add_argument("--dp-mode", default="p2p", choices=["nccl", "p2p", "nvls"],
+                    help="N>1 collectives: NCCL RS/AG, or fused kernels over NVLink peer memory "
+                         "(p2p) / NVSwitch multicast (nvls)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-pages", type=int, default=32)

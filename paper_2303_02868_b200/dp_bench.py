@@ -59,13 +59,15 @@ def _max_over_ranks(x: float) -> float:
 def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     from . import lockfree as LF
     from . import workloads as W
-    from .sharding import ShardedPageStep
+    from .sharding import FusedShardedPageStep, ShardedPageStep, symmetric_alloc
     rank, world, device = _init()
-    specs, page, layout, buf, ms = build_state(args, device, world, rank)
+    fused = args.dp_mode != "nccl"
+    specs, page, layout, buf, ms = build_state(args, device, world, rank,
+                                               pool_alloc=symmetric_alloc if fused else None)
     L = len(specs)
     P = sum(layout.numels)
     hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
-    dp = ShardedPageStep(buf, ms)
+    dp = FusedShardedPageStep(buf, ms, mode=args.dp_mode) if fused else ShardedPageStep(buf, ms)
     flat = owned_grad_flat(layout, args.dtype, device, 7 + rank)
     for rnd in range(2):  # fill both gradient page buffers (K3)
         buf.accumulate_flat(flat, rnd)
@@ -119,8 +121,12 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         torch.cuda.synchronize()
         return _max_over_ranks(a.elapsed_time(b) / reps)
 
-    rs_ms = timed(lambda: dp.coll.reduce_scatter(gpool))
-    ag_ms = timed(lambda: dp.coll.all_gather(ppool))
+    if fused:  # the collectives live inside the kernels: use the instrumented step
+        rs_ms = parts["rs_ms"]
+        ag_ms = parts["adam_ms"] + parts["ag_tail_ms"]
+    else:
+        rs_ms = timed(lambda: dp.coll.reduce_scatter(gpool))
+        ag_ms = timed(lambda: dp.coll.all_gather(ppool))
     pool_bytes = layout.elems16 * 2
     busbw = lambda ms_: pool_bytes / (ms_ / 1e3) * (world - 1) / world / 1e9
     # Sharded page-Adam alone (owned pages) for the HBM roofline.
@@ -137,19 +143,25 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "page_bytes": page, "pages": layout.used_pages, "bucket_pages_per_rank": layout.K,
                    "buckets": layout.num_buckets, "parallelism": f"dp{world} (page-sharded ZeRO-3)",
                    "l2": "inputs larger than L2",
-                   "step": "RS(grad pages) -> check -> flag all-reduce -> prologue -> "
-                           "page-Adam(bucket) || AG(bucket)"},
+                   "dp_mode": args.dp_mode,
+                   "step": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
+                            "page-Adam(bucket) || AG(bucket)") if not fused else
+                           ("barrier -> fused reduce-scatter+check over peer memory -> barrier -> "
+                            "flag merge -> prologue -> page-Adam with all-gather epilogue -> barrier")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "peak_kind": peak_kind,
                      "traffic": None, "kernel": "adam_main on owned pages (instrumented step, "
                                                 "overlapped with AG)", "kernel_ms": adam_ms},
-        "nvlink": {"rs_ms": rs_ms, "ag_ms": ag_ms, "rs_busbw_gbs": busbw(rs_ms), "ag_busbw_gbs": busbw(ag_ms),
+        "nvlink": {"rs_ms": rs_ms, "ag_ms": ag_ms,
+                   "note": ("isolated NCCL collectives" if not fused else
+                            "fused kernels: rs = reduce+check kernel; ag = page-Adam with the all-gather "
+                            "epilogue (includes the update) + final barrier"), "rs_busbw_gbs": busbw(rs_ms), "ag_busbw_gbs": busbw(ag_ms),
                    "peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                    "nominal_gbs": 900.0, "rs_frac": busbw(rs_ms) / 770.0, "ag_frac": busbw(ag_ms) / 770.0,
                    "pool_bytes": pool_bytes},
         "components_ms": parts,
         "clocks": clk.summary(),
-        "gpu_launches": args.steps * (2 + layout.num_buckets),
+        "gpu_launches": args.steps * ((2 + layout.num_buckets) if not fused else 4),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
