@@ -49,6 +49,7 @@ def main():
     om = O.OracleMasters(params)
     hyper = LF.AdamHyper(lr=1e-3)
     failures = []
+    stats = {}
     if mode != "nccl":
         print(f"rank {rank}: fused mode {mode}, mc={getattr(step, 'mc_g', 0)}", flush=True)
     for it in range(3):
@@ -94,11 +95,20 @@ def main():
                 if world == 2 or mode == "p2p":
                     if not np.array_equal(got.view(np.uint16), want.view(np.uint16)):
                         failures.append(f"it{it} layer{l}: reduced grad differs from oracle sum")
-                else:
+                else:   # NCCL ring at N>2 / NVLS in-switch reduction: within one 16-bit ulp
                     gf, wf = O.from16(got, dtype), O.from16(want, dtype)
                     fin = np.isfinite(wf)
-                    if not np.allclose(gf[fin], wf[fin], rtol=2 ** -7, atol=1e-30):
-                        failures.append(f"it{it} layer{l}: reduced grad off by > 1 bf16 ulp")
+                    ulp = 2.0 ** -7 if dtype == "bf16" else 2.0 ** -10
+                    if fin.any():
+                        rel = np.abs(gf[fin] - wf[fin]) / np.maximum(np.abs(wf[fin]), 1e-30)
+                        worst = float(rel.max())
+                        stats["max_rel"] = max(stats.get("max_rel", 0.0), worst)
+                        stats["mismatch"] = stats.get("mismatch", 0) + int((gf[fin] != wf[fin]).sum())
+                        stats["n"] = stats.get("n", 0) + int(fin.sum())
+                        if worst > ulp:
+                            failures.append(f"it{it} layer{l}: reduced grad off by {worst:.3g} > 1 ulp")
+                    if np.isfinite(gf).sum() != fin.sum():
+                        failures.append(f"it{it} layer{l}: non-finite pattern differs")
                 captured[s.pos:s.pos + s.n] = got
             # oracle Adam on the captured reduced gradient
             om.update_layer(l, O.from16(captured, dtype), lr=1e-3)
@@ -118,6 +128,8 @@ def main():
                 failures.append(f"layer{l} page{s.page}: owned p32 differs")
     ok = torch.tensor([0 if failures else 1], device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if stats:
+        print(f"rank {rank}: reduced-gradient deviation vs f32-sum oracle: {stats}", flush=True)
     if failures:
         print(f"rank {rank} FAIL:", *failures[:10], sep="\n  ")
     dist.destroy_process_group()
