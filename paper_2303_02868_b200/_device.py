@@ -4,6 +4,7 @@ holds the exact bias-correction tables.  No compute happens here."""
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from collections import OrderedDict
 
 import numpy as np
@@ -52,11 +53,14 @@ class DescCache:
         self._lru_cap = lru
 
     def static(self, arr: np.ndarray) -> torch.Tensor:
-        hit = self._static.get(id(arr))
-        if hit is not None and hit[0] is arr:
+        key = id(arr)
+        hit = self._static.get(key)
+        if hit is not None and hit[0]() is arr:
             return hit[1]
         dev = self._upload(arr)
-        self._static[id(arr)] = (arr, dev)
+        # the device copy lives exactly as long as the host plan it mirrors
+        self._static[key] = (weakref.ref(arr), dev)
+        weakref.finalize(arr, self._static.pop, key, None)
         return dev
 
     def table(self, arr: np.ndarray) -> torch.Tensor:

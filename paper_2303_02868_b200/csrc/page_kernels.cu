@@ -11,14 +11,21 @@
 namespace hm {
 namespace {
 
+// The segment kernels below stream 2-6 B/param with little math, so they
+// need many bytes in flight per thread: 128 threads x 4 granules per
+// 4096-element chunk (vs 256 x 2 for the register-heavy page-Adam).
+constexpr int kSegThreads = 128;
+constexpr int kSegVecPer = kChunk / (kSegThreads * kVec);
+static_assert(kSegVecPer * kSegThreads * kVec == kChunk, "segment chunk geometry");
+
 // Flush of the fused statistics: warp shuffles, ONE block barrier, then one
 // atomic per CTA (per-warp f64 atomics on a few hundred layer addresses
 // serialise in L2 and cost 3x in measurement).  sumsq feeds the grad norm /
 // clip only, so its f64 atomic order is free to vary.
 __device__ __forceinline__ void flush_stats(bool bad, float sq, uint32_t* nonfinite, double* sumsq,
                                             uint32_t slot) {
-  __shared__ float s_sq[kThreads / 32];
-  __shared__ int s_bad[kThreads / 32];
+  __shared__ float s_sq[kSegThreads / 32];
+  __shared__ int s_bad[kSegThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -32,7 +39,7 @@ __device__ __forceinline__ void flush_stats(bool bad, float sq, uint32_t* nonfin
     float t = 0.f;
     int b = 0;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
+    for (int w = 0; w < kSegThreads / 32; ++w) {
       t += s_sq[w];
       b |= s_bad[w];
     }
@@ -45,7 +52,7 @@ __device__ __forceinline__ void flush_stats(bool bad, float sq, uint32_t* nonfin
 // sumsq accumulates sum(new^2 - old^2) so that it telescopes to the squared
 // norm of the final buffer over any number of messages.
 template <int SDT, int DDT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kSegThreads)
 accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
                   void* __restrict__ dst, int mode, const uint8_t* __restrict__ slot_modes,
                   uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq) {
@@ -56,10 +63,10 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
   float sq = 0.f;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
-    F8 a[kVecPerThread], b[kVecPerThread];
+    F8 a[kSegVecPer], b[kSegVecPer];
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e < c.n) {
         load8_ro<SDT>(src, c.src_off + e, a[k]);
         if (add) load8_rw<DDT>(dst, c.dst_off + e, b[k]);
@@ -70,8 +77,8 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
       }
     }
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e >= c.n) continue;
       F8 o;
 #pragma unroll
@@ -84,7 +91,7 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
       store8<DDT>(dst, c.dst_off + e, o);
     }
   } else {
-    for (uint32_t i = tid; i < c.n; i += kThreads) {
+    for (uint32_t i = tid; i < c.n; i += kSegThreads) {
       const float a1 = load1<SDT>(src, c.src_off + i);
       const float b1 = add ? load1<DDT>(dst, c.dst_off + i) : 0.0f;
       const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b1, a1)));
@@ -97,51 +104,51 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
 }
 
 template <int SDT, int DDT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kSegThreads)
 cast_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
             void* __restrict__ dst) {
   const hm_seg_chunk c = chunks[blockIdx.x];
   const int tid = threadIdx.x;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
-    F8 a[kVecPerThread];
+    F8 a[kSegVecPer];
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e < c.n) load8_ro<SDT>(src, c.src_off + e, a[k]);
     }
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e < c.n) store8<DDT>(dst, c.dst_off + e, a[k]);
     }
   } else {
-    for (uint32_t i = tid; i < c.n; i += kThreads)
+    for (uint32_t i = tid; i < c.n; i += kSegThreads)
       store1<DDT>(dst, c.dst_off + i, load1<SDT>(src, c.src_off + i));
   }
 }
 
 template <int SDT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kSegThreads)
 reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
               uint32_t* __restrict__ nonfinite, double* __restrict__ sums,
               double* __restrict__ sumsq) {
-  __shared__ double red[kThreads / 32];
+  __shared__ double red[kSegThreads / 32];
   const hm_seg_chunk c = chunks[blockIdx.x];
   const int tid = threadIdx.x;
   bool bad = false;
   double s = 0.0, sq = 0.0;
   const bool vec = ((c.src_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
-    F8 a[kVecPerThread];
+    F8 a[kSegVecPer];
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e < c.n) load8_ro<SDT>(src, c.src_off + e, a[k]);
     }
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e >= c.n) continue;
 #pragma unroll
       for (int j = 0; j < kVec; ++j) {
@@ -152,7 +159,7 @@ reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ 
       }
     }
   } else {
-    for (uint32_t i = tid; i < c.n; i += kThreads) {
+    for (uint32_t i = tid; i < c.n; i += kSegThreads) {
       const float x = load1<SDT>(src, c.src_off + i);
       bad |= !is_finite(x);
       s += (double)x;
@@ -160,7 +167,7 @@ reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ 
     }
   }
   if (sums) {
-    const double tot = block_sum<kThreads>(s, red);
+    const double tot = block_sum<kSegThreads>(s, red);
     if (threadIdx.x == 0) atomicAdd(&sums[c.slot], tot);
   }
   flush_stats(bad, (float)sq, nonfinite, sumsq, c.slot);
@@ -293,7 +300,7 @@ int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
   hm::AccFn fn = hm::pick_acc(src_dtype, dst_dtype);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_accumulate: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
   if (n_chunks == 0) return HM_OK;
-  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, src, dst, mode ? 1 : 0, slot_modes, nonfinite, sumsq);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
@@ -305,7 +312,7 @@ int hm_cast(const void* src, int src_dtype, void* dst, int dst_dtype, const hm_s
   hm::CastFn fn = hm::pick_cast(src_dtype, dst_dtype);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_cast: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
   if (n_chunks == 0) return HM_OK;
-  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, dst);
+  fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, dst);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }
@@ -316,7 +323,7 @@ int hm_reduce_stats(const void* src, int src_dtype, const hm_seg_chunk* chunks, 
   hm::RedFn fn = hm::pick_red(src_dtype);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_reduce_stats: unsupported dtype %d", src_dtype);
   if (n_chunks == 0) return HM_OK;
-  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, nonfinite,
+  fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, nonfinite,
                                                                                  sums, sumsq);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;

@@ -440,6 +440,23 @@ class ParamBuffer(_Paged):
             return self._out(t, layer)
         return self._unpack16(self.g16_pool[self._gsel[layer]], layer)
 
+    def layer_view(self, layer: int, buf: int | None = None, *, stream=None) -> torch.Tensor:
+        """The layer's 16-bit parameters in published buffer ``buf`` (default:
+        the current record) as a CUDA tensor of the layer's shape: a zero-copy
+        view when its page segments are contiguous in the pool (tensors
+        allocated in order usually are), otherwise an unpacked copy."""
+        buf = self._psel[layer] if buf is None else buf
+        lay = self.layout
+        segs = lay.segments[layer]
+        base = lay.slot16(segs[0].page) * lay.E + segs[0].off
+        pos = base
+        for s in segs:
+            if lay.slot16(s.page) * lay.E + s.off != pos:
+                return self._unpack16(self.p16_pool[buf], layer, stream=stream, raw=True).view(
+                    self._shapes[layer])
+            pos += s.n
+        return self.p16_pool[buf][base:pos].view(self._shapes[layer])
+
     def _unpack16(self, pool, layer, readonly=False, stream=None, raw=False):
         st = self._stream(stream)
         with torch.cuda.stream(st):

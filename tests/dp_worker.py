@@ -95,18 +95,24 @@ def main():
                 if world == 2 or mode == "p2p":
                     if not np.array_equal(got.view(np.uint16), want.view(np.uint16)):
                         failures.append(f"it{it} layer{l}: reduced grad differs from oracle sum")
-                else:   # NCCL ring at N>2 / NVLS in-switch reduction: within one 16-bit ulp
+                else:   # NCCL ring at N>2 / NVLS in-switch reduction: 16-bit rounding bound
+                    # Each of the N-1 additions may round by half an ulp of a partial
+                    # sum, and every partial sum is bounded by sum_r |g_r|.
                     gf, wf = O.from16(got, dtype), O.from16(want, dtype)
                     fin = np.isfinite(wf)
-                    ulp = 2.0 ** -7 if dtype == "bf16" else 2.0 ** -10
+                    u = 2.0 ** -8 if dtype == "bf16" else 2.0 ** -11
                     if fin.any():
-                        rel = np.abs(gf[fin] - wf[fin]) / np.maximum(np.abs(wf[fin]), 1e-30)
-                        worst = float(rel.max())
-                        stats["max_rel"] = max(stats.get("max_rel", 0.0), worst)
+                        absum = np.zeros(s.n, np.float32)
+                        for r in range(world):
+                            absum += np.abs(O.from16(per_rank[r][l][s.pos:s.pos + s.n], dtype))
+                        bound = (world - 1) * u * absum[fin] + 1e-38
+                        err = np.abs(gf[fin] - wf[fin])
+                        worst = float((err / bound).max())
+                        stats["max_err_over_bound"] = max(stats.get("max_err_over_bound", 0.0), worst)
                         stats["mismatch"] = stats.get("mismatch", 0) + int((gf[fin] != wf[fin]).sum())
                         stats["n"] = stats.get("n", 0) + int(fin.sum())
-                        if worst > ulp:
-                            failures.append(f"it{it} layer{l}: reduced grad off by {worst:.3g} > 1 ulp")
+                        if worst > 1.0:
+                            failures.append(f"it{it} layer{l}: reduced grad error {worst:.3g}x the rounding bound")
                     if np.isfinite(gf).sum() != fin.sum():
                         failures.append(f"it{it} layer{l}: non-finite pattern differs")
                 captured[s.pos:s.pos + s.n] = got
