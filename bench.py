@@ -355,10 +355,14 @@ def main():
     ap.add_argument("--cpu-sample-pages", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c3-layers", type=int, default=8, help="C3 slice (host-memory bound)")
+    ap.add_argument("--adam-threads", type=int, default=256, choices=[256, 512])
     ap.add_argument("--swap-group-pages", type=int, default=64)
     ap.add_argument("--swap-slots", type=int, default=2)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.impl != "reference":
+        from paper_2303_02868_b200 import _native
+        _native.check(_native.lib().hm_set_adam_threads(args.adam_threads))
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "c3":

@@ -175,6 +175,10 @@ int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                  uint32_t* nonfinite, double* sumsq, int consume_flags,
                  void* stream);
 
+/* Tuning knob of the page-Adam main kernel: 256 (default) or 512 threads per
+ * 4096-element chunk (2 or 1 granule of 8 elements per thread).  Process-wide. */
+int hm_set_adam_threads(int threads);
+
 /* The two halves of hm_adam_step, for callers that pipeline the main pass
  * (e.g. per all-gather bucket) after ONE prologue over every group: the
  * prologue must run exactly once per update or steps[] would advance twice. */

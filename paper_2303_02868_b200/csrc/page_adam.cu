@@ -131,8 +131,10 @@ __device__ __forceinline__ void publish1(void* p16, const PeerPtrs& peers, uint6
   }
 }
 
-template <int GDT, int PDT, int PUB = kPubLocal>
-__global__ void __launch_bounds__(kThreads)
+// NT threads per 4096-element chunk: 256 (2 granules/thread, all 7 loads of
+// both issued up front) or 512 (1 granule/thread, more warps to hide latency).
+template <int GDT, int PDT, int PUB = kPubLocal, int NT = kThreads>
+__global__ void __launch_bounds__(NT)
 adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ groups,
           const hm_group_rt* __restrict__ rt, const void* __restrict__ g,
           float* __restrict__ p32, float* __restrict__ m32, float* __restrict__ v32,
@@ -150,7 +152,7 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
   if (!r.apply) {
     // Rejected layer: state untouched; still publish the unchanged masters.
     if constexpr (kPub) {
-      for (uint32_t i = tid; i < n; i += kThreads) publish1<PDT, PUB>(p16, peers, po + i, p32[so + i]);
+      for (uint32_t i = tid; i < n; i += NT) publish1<PDT, PUB>(p16, peers, po + i, p32[so + i]);
     }
     return;
   }
@@ -169,11 +171,12 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
   if (vec) {
     // Issue every load of the thread's 2 granules before any math: 2 x
     // (16 B g + 3 x 32 B state) in flight per thread.
-    F8 gv[kVecPerThread], pv[kVecPerThread], mv[kVecPerThread], vv[kVecPerThread];
-    bool live[kVecPerThread];
+    constexpr int VPT = kChunk / (NT * kVec);
+    F8 gv[VPT], pv[VPT], mv[VPT], vv[VPT];
+    bool live[VPT];
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+    for (int k = 0; k < VPT; ++k) {
+      const uint32_t e = (uint32_t)(k * NT + tid) * kVec;
       live[k] = e < n;
       if (live[k]) {
         load8_ro<GDT>(g, go + e, gv[k]);
@@ -183,9 +186,9 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
       }
     }
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
+    for (int k = 0; k < VPT; ++k) {
       if (!live[k]) continue;
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      const uint32_t e = (uint32_t)(k * NT + tid) * kVec;
 #pragma unroll
       for (int j = 0; j < kVec; ++j) adam_elem(s, gv[k].v[j], pv[k].v[j], mv[k].v[j], vv[k].v[j]);
       store8<HM_DT_F32>(p32, so + e, pv[k]);
@@ -194,7 +197,7 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
       if constexpr (kPub) publish8<PDT, PUB>(p16, peers, mc, po + e, pv[k]);
     }
   } else {
-    for (uint32_t i = tid; i < n; i += kThreads) {
+    for (uint32_t i = tid; i < n; i += NT) {
       float gg = load1<GDT>(g, go + i);
       float p = p32[so + i], m = m32[so + i], v = v32[so + i];
       adam_elem(s, gg, p, m, v);
@@ -219,23 +222,30 @@ AdamFn pick_adam_ag(int gdt, int pdt, int pub) {
                           : adam_main<HM_DT_F16, HM_DT_F16, kPubMulticast>;
 }
 
-template <int GDT>
+int g_adam_threads = kThreads;  // tuning knob: hm_set_adam_threads
+
+template <int GDT, int NT>
 AdamFn pick_p(int pdt) {
   switch (pdt) {
-    case 0: return adam_main<GDT, 0>;
-    case HM_DT_F16: return adam_main<GDT, HM_DT_F16>;
-    case HM_DT_BF16: return adam_main<GDT, HM_DT_BF16>;
+    case 0: return adam_main<GDT, 0, kPubLocal, NT>;
+    case HM_DT_F16: return adam_main<GDT, HM_DT_F16, kPubLocal, NT>;
+    case HM_DT_BF16: return adam_main<GDT, HM_DT_BF16, kPubLocal, NT>;
+  }
+  return nullptr;
+}
+
+template <int NT>
+AdamFn pick_adam_nt(int gdt, int pdt) {
+  switch (gdt) {
+    case HM_DT_F16: return pick_p<HM_DT_F16, NT>(pdt);
+    case HM_DT_BF16: return pick_p<HM_DT_BF16, NT>(pdt);
+    case HM_DT_F32: return pick_p<HM_DT_F32, NT>(pdt);
   }
   return nullptr;
 }
 
 AdamFn pick_adam(int gdt, int pdt) {
-  switch (gdt) {
-    case HM_DT_F16: return pick_p<HM_DT_F16>(pdt);
-    case HM_DT_BF16: return pick_p<HM_DT_BF16>(pdt);
-    case HM_DT_F32: return pick_p<HM_DT_F32>(pdt);
-  }
-  return nullptr;
+  return g_adam_threads == 512 ? pick_adam_nt<512>(gdt, pdt) : pick_adam_nt<kThreads>(gdt, pdt);
 }
 
 }  // namespace
@@ -281,9 +291,16 @@ extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (n_chunks == 0) return HM_OK;
   hm::PeerPtrs none{};
-  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  fn<<<(unsigned)n_chunks, hm::g_adam_threads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, groups, rt, g, p32, m32, v32, p16, *hyper, none, nullptr);
   HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+extern "C" int hm_set_adam_threads(int threads) {
+  if (threads != 256 && threads != 512)
+    return hm_set_error(HM_ERR_INVALID, "hm_set_adam_threads: 256 or 512, got %d", threads);
+  hm::g_adam_threads = threads;
   return HM_OK;
 }
 
