@@ -280,6 +280,7 @@ def run_ours_single(args):
         "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": P,
                    "layers": L, "page_bytes": page, "pages": layout.used_pages,
+                   "adam_threads": args.adam_threads,
                    "l2": "inputs larger than L2 (28 B/param x params >> 126 MB)",
                    "step": "fused sweep: prologue + page-Adam over all pages (take->update->publish)"},
         "hbm_gbs": achieved,

@@ -188,3 +188,51 @@ class DevicePageManager(PageManager):
             for (a0, a1, n), buf in zip(moves, tmp):
                 store[a1:a1 + n].copy_(buf)
         return report
+
+
+def _flat_runs(dm: "DevicePageManager", tensor_ids, reverse: bool):
+    """All GPU-tier runs of many tensors against one flat buffer (tensor order)."""
+    rows, base = [], 0
+    for tid in tensor_ids:
+        t = dm.tensors[tid]
+        pos = 0
+        for pid, off, nbytes in t.segments():
+            tier, addr = dm._loc(pid)
+            if tier is not Tier.GPU:
+                raise ConfigError("batched pack/unpack covers GPU pages; move CPU pages first")
+            rows.append((addr + off, base + pos, nbytes) if reverse else (base + pos, addr + off, nbytes))
+            pos += nbytes
+        base += t.bytes
+    return rows, base
+
+
+def pack_many(dm: "DevicePageManager", tensor_ids, flat: torch.Tensor, *, stream=None) -> None:
+    """Pack many tensors, stored back to back in ``flat``, with ONE launch (K1)."""
+    key = ("pack", tuple(tensor_ids))
+    cache = dm.__dict__.setdefault("_batch_cache", {})
+    if key not in cache:
+        rows, total = _flat_runs(dm, tensor_ids, reverse=False)
+        d = _descs(rows)
+        cache[key] = (dm._up(d), len(d), total)
+    dd, n, total = cache[key]
+    raw = flat.reshape(-1).view(torch.uint8)
+    if raw.numel() != total:
+        raise ConfigError(f"flat buffer holds {raw.numel()} bytes, tensors need {total}")
+    st = D.cur_stream(dm.device, stream)
+    D.check(N.lib().hm_copy_runs(D.ptr(raw), D.ptr(dm.storage[Tier.GPU]), D.ptr(dd), n, D.sptr(st)))
+
+
+def unpack_many(dm: "DevicePageManager", tensor_ids, *, stream=None) -> torch.Tensor:
+    """Unpack many tensors back to back into one flat uint8 CUDA tensor (K1)."""
+    key = ("unpack", tuple(tensor_ids))
+    cache = dm.__dict__.setdefault("_batch_cache", {})
+    if key not in cache:
+        rows, total = _flat_runs(dm, tensor_ids, reverse=True)
+        d = _descs(rows)
+        cache[key] = (dm._up(d), len(d), total)
+    dd, n, total = cache[key]
+    st = D.cur_stream(dm.device, stream)
+    with torch.cuda.stream(st):
+        out = torch.empty(total, dtype=torch.uint8, device=dm.device)
+    D.check(N.lib().hm_copy_runs(D.ptr(dm.storage[Tier.GPU]), D.ptr(out), D.ptr(dd), n, D.sptr(st)))
+    return out
