@@ -64,6 +64,7 @@ class LockFreeRunner:
         from .swap import HostMasterState, swap_sweep
         self._sweep = swap_sweep if isinstance(masters, HostMasterState) else sweep
         self._pub: list[tuple[torch.cuda.Event, int, int]] = []   # (event, psel, version)
+        self._it = 0                  # global iteration counter across run() calls
         self._psel0 = buffer._psel[0]
         if any(p != self._psel0 for p in buffer._psel):
             raise ConfigError("all layers must start in the same published buffer")
@@ -88,7 +89,9 @@ class LockFreeRunner:
         losses = []
         torch.cuda.synchronize(self.buffer.device)
         t0 = time.perf_counter()
-        for it in range(iterations):
+        for _ in range(iterations):
+            it = self._it
+            self._it += 1
             with torch.cuda.stream(self.cs):
                 params, src = self.params(it)
                 applied = -1 if src < 0 else src

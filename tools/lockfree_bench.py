@@ -31,8 +31,10 @@ def main():
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--state", default="host", choices=["host", "hbm"])
+    ap.add_argument("--tf32", action="store_true", help="TF32 tensor-core matmuls in the GPU actor")
     args = ap.parse_args()
-    out = {"layers": args.layers, "dim": args.dim, "batch": args.batch, "iters": args.iters,
+    torch.backends.cuda.matmul.allow_tf32 = args.tf32
+    out = {"layers": args.layers, "dim": args.dim, "batch": args.batch, "iters": args.iters, "tf32": args.tf32,
            "params": args.layers * args.dim * args.dim, "state": args.state}
     hyper = LF.AdamHyper(lr=1e-4)
     for delay in (0, 1):
