@@ -143,6 +143,40 @@ __device__ __forceinline__ void store8(void* base, uint64_t off, const F8& r) {
   }
 }
 
+// Raw (undecoded) 8-element granules: issue every load of a thread first and
+// decode afterwards, so no use sits between two loads (the compiler otherwise
+// serialises load -> convert -> next load when a load is conditional).
+template <int DT>
+struct Raw8 {
+  uint4 u;
+};
+template <>
+struct Raw8<HM_DT_F32> {
+  F8 f;
+};
+
+template <int DT>
+__device__ __forceinline__ void ld_raw_ro(const void* base, uint64_t off, Raw8<DT>& r) {
+  if constexpr (DT == HM_DT_F32) ld_ro_f8(static_cast<const float*>(base) + off, r.f);
+  else r.u = ld_stream_u4(static_cast<const typename Elem<DT>::T*>(base) + off);
+}
+template <int DT>
+__device__ __forceinline__ void ld_raw_rw(const void* base, uint64_t off, Raw8<DT>& r) {
+  if constexpr (DT == HM_DT_F32) ld_stream_f8(static_cast<const float*>(base) + off, r.f);
+  else r.u = *reinterpret_cast<const uint4*>(static_cast<const typename Elem<DT>::T*>(base) + off);
+}
+template <int DT>
+__device__ __forceinline__ void decode(const Raw8<DT>& r, F8& out) {
+  if constexpr (DT == HM_DT_F32) {
+    out = r.f;
+  } else {
+    using T = typename Elem<DT>::T;
+    const T* h = reinterpret_cast<const T*>(&r.u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out.v[i] = Elem<DT>::widen(h[i]);
+  }
+}
+
 __device__ __forceinline__ bool is_finite(float x) { return isfinite(x); }
 
 // Deterministic block reduction of a double (fixed tree order).

@@ -172,14 +172,18 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
     // Issue every load of the thread's 2 granules before any math: 2 x
     // (16 B g + 3 x 32 B state) in flight per thread.
     constexpr int VPT = kChunk / (NT * kVec);
-    F8 gv[VPT], pv[VPT], mv[VPT], vv[VPT];
+    // Raw loads of every granule first (4 per granule: g 128-bit, p/m/v
+    // 256-bit), decode afterwards: no use between two loads, so all of a
+    // thread's loads are in flight together.
+    Raw8<GDT> graw[VPT];
+    F8 pv[VPT], mv[VPT], vv[VPT];
     bool live[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const uint32_t e = (uint32_t)(k * NT + tid) * kVec;
       live[k] = e < n;
       if (live[k]) {
-        load8_ro<GDT>(g, go + e, gv[k]);
+        ld_raw_ro<GDT>(g, go + e, graw[k]);
         load8_rw<HM_DT_F32>(p32, so + e, pv[k]);
         load8_rw<HM_DT_F32>(m32, so + e, mv[k]);
         load8_rw<HM_DT_F32>(v32, so + e, vv[k]);
@@ -189,8 +193,10 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
     for (int k = 0; k < VPT; ++k) {
       if (!live[k]) continue;
       const uint32_t e = (uint32_t)(k * NT + tid) * kVec;
+      F8 gk;
+      decode<GDT>(graw[k], gk);
 #pragma unroll
-      for (int j = 0; j < kVec; ++j) adam_elem(s, gv[k].v[j], pv[k].v[j], mv[k].v[j], vv[k].v[j]);
+      for (int j = 0; j < kVec; ++j) adam_elem(s, gk.v[j], pv[k].v[j], mv[k].v[j], vv[k].v[j]);
       store8<HM_DT_F32>(p32, so + e, pv[k]);
       store8<HM_DT_F32>(m32, so + e, mv[k]);
       store8<HM_DT_F32>(v32, so + e, vv[k]);

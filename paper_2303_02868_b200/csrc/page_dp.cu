@@ -94,27 +94,37 @@ reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, PeerPtrs peers, con
   float sq = 0.f;
   const bool vec = ((off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
+    // Every remote load of the thread (granules x peers) is issued before
+    // any of them is consumed: NVLink latency (~2 us) needs the depth.
+    uint4 u[kVecPerThread][MC ? 1 : kMaxPeers];
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+      if (e >= c.n) continue;
+      if constexpr (MC) {
+        u[k][0] = ld_reduce_mc<DT>(mc + (off + e) * sizeof(T));
+      } else {
+#pragma unroll
+        for (int r = 0; r < kMaxPeers; ++r)
+          if (r < peers.n) u[k][r] = ld_peer_u4(reinterpret_cast<const T*>(peers.p[r]) + off + e);
+      }
+    }
 #pragma unroll
     for (int k = 0; k < kVecPerThread; ++k) {
       const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
       if (e >= c.n) continue;
       F8 acc;
       if constexpr (MC) {
-        uint4 u = ld_reduce_mc<DT>(mc + (off + e) * sizeof(T));
-        const T* h = reinterpret_cast<const T*>(&u);
+        const T* h = reinterpret_cast<const T*>(&u[k][0]);
 #pragma unroll
         for (int j = 0; j < kVec; ++j) acc.v[j] = Elem<DT>::widen(h[j]);
       } else {
-        uint4 u[kMaxPeers];
-#pragma unroll
-        for (int r = 0; r < kMaxPeers; ++r)
-          if (r < peers.n) u[r] = ld_peer_u4(reinterpret_cast<const T*>(peers.p[r]) + off + e);
 #pragma unroll
         for (int j = 0; j < kVec; ++j) acc.v[j] = 0.f;
 #pragma unroll
         for (int r = 0; r < kMaxPeers; ++r) {
           if (r >= peers.n) break;
-          const T* h = reinterpret_cast<const T*>(&u[r]);
+          const T* h = reinterpret_cast<const T*>(&u[k][r]);
 #pragma unroll
           for (int j = 0; j < kVec; ++j) acc.v[j] = __fadd_rn(acc.v[j], Elem<DT>::widen(h[j]));
         }

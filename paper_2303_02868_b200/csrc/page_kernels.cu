@@ -63,29 +63,41 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
   float sq = 0.f;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
-    F8 a[kSegVecPer], b[kSegVecPer];
+    // All raw loads first (one straight-line batch per mode), decode after.
+    Raw8<SDT> ra[kSegVecPer];
+    Raw8<DDT> rb[kSegVecPer];
+    if (add) {
 #pragma unroll
-    for (int k = 0; k < kSegVecPer; ++k) {
-      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-      if (e < c.n) {
-        load8_ro<SDT>(src, c.src_off + e, a[k]);
-        if (add) load8_rw<DDT>(dst, c.dst_off + e, b[k]);
-        else {
-#pragma unroll
-          for (int j = 0; j < kVec; ++j) b[k].v[j] = 0.0f;
+      for (int k = 0; k < kSegVecPer; ++k) {
+        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
+        if (e < c.n) {
+          ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
+          ld_raw_rw<DDT>(dst, c.dst_off + e, rb[k]);
         }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kSegVecPer; ++k) {
+        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
+        if (e < c.n) ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
       }
     }
 #pragma unroll
     for (int k = 0; k < kSegVecPer; ++k) {
       const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e >= c.n) continue;
-      F8 o;
+      F8 a, b, o;
+      decode<SDT>(ra[k], a);
+      if (add) decode<DDT>(rb[k], b);
+      else {
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) b.v[j] = 0.0f;
+      }
 #pragma unroll
       for (int j = 0; j < kVec; ++j) {
-        const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b[k].v[j], a[k].v[j])));
+        const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b.v[j], a.v[j])));
         bad |= !is_finite(r);
-        if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b[k].v[j], b[k].v[j]));
+        if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b.v[j], b.v[j]));
         o.v[j] = r;
       }
       store8<DDT>(dst, c.dst_off + e, o);

@@ -47,7 +47,6 @@ def test_sync_runner_equals_sequential_loop(cuda):
         assert torch.equal(buf.layer_view(l).view(torch.int16), b2.layer_view(l).view(torch.int16))
 
 
-@pytest.mark.parametrize("swap", [False, True])
 def test_runner_is_reentrant(cuda):
     """Two run() calls continue one iteration sequence (warm-up then timed run)."""
     toy = ToyMLP(num_layers=2, dim=32, batch_size=32, seed=2)
@@ -61,6 +60,7 @@ def test_runner_is_reentrant(cuda):
     assert len(a) == 7 and all(s == 7 for s in m1.steps)
 
 
+@pytest.mark.parametrize("swap", [False, True])
 def test_lockfree_runner_bounded_staleness_and_convergence(cuda, swap):
     toy = ToyMLP(num_layers=4, dim=64, batch_size=64, seed=1, noise_std=0.01)
     # lr 1e-3: a one-step-stale Adam at lr 1e-2 diverges on this toy in exact
