@@ -123,16 +123,19 @@ cast_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ sr
   const int tid = threadIdx.x;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
-    F8 a[kSegVecPer];
+    Raw8<SDT> ra[kSegVecPer];
 #pragma unroll
     for (int k = 0; k < kSegVecPer; ++k) {
       const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-      if (e < c.n) load8_ro<SDT>(src, c.src_off + e, a[k]);
+      if (e < c.n) ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
     }
 #pragma unroll
     for (int k = 0; k < kSegVecPer; ++k) {
       const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-      if (e < c.n) store8<DDT>(dst, c.dst_off + e, a[k]);
+      if (e >= c.n) continue;
+      F8 a;
+      decode<SDT>(ra[k], a);
+      store8<DDT>(dst, c.dst_off + e, a);
     }
   } else {
     for (uint32_t i = tid; i < c.n; i += kSegThreads)
@@ -152,19 +155,21 @@ reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ 
   double s = 0.0, sq = 0.0;
   const bool vec = ((c.src_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
-    F8 a[kSegVecPer];
+    Raw8<SDT> ra[kSegVecPer];
 #pragma unroll
     for (int k = 0; k < kSegVecPer; ++k) {
       const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-      if (e < c.n) load8_ro<SDT>(src, c.src_off + e, a[k]);
+      if (e < c.n) ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
     }
 #pragma unroll
     for (int k = 0; k < kSegVecPer; ++k) {
       const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
       if (e >= c.n) continue;
+      F8 a;
+      decode<SDT>(ra[k], a);
 #pragma unroll
       for (int j = 0; j < kVec; ++j) {
-        const float x = a[k].v[j];
+        const float x = a.v[j];
         bad |= !is_finite(x);
         s += (double)x;
         sq += (double)x * (double)x;
