@@ -689,3 +689,94 @@ def sweep(buffer: ParamBuffer, masters: MasterState, hyper: AdamHyper, layers=No
         for l in sel:
             buffer.ledger.record_apply(l, buffer.ledger.consumed_sums[l][-1], rejected=not ok[l])
     return SweepResult(masters, sel, counts, newest)
+
+
+class _MultiResult(SweepResult):
+    def __init__(self, masters, parts):
+        super().__init__(masters, [l for p in parts for l in p.layers],
+                         [c for p in parts for c in p.counts], [n for p in parts for n in p.newest])
+
+
+def layer_groups(numels, groups: int) -> list[list[int]]:
+    """Contiguous layer ranges of about equal element count."""
+    total = sum(numels)
+    out, cur, acc = [], [], 0
+    for l, n in enumerate(numels):
+        cur.append(l)
+        acc += n
+        if acc >= total * (len(out) + 1) / groups and len(out) < groups - 1:
+            out.append(cur)
+            cur = []
+    if cur:
+        out.append(cur)
+    return out
+
+
+def ingest_sweep(buffer: ParamBuffer, masters: MasterState, host_grad, hyper: AdamHyper,
+                 iteration: int = 0, *, groups: int = 8, stream=None, copy_stream=None) -> SweepResult:
+    """One update step fed by a flat gradient in (pinned) host memory — what a
+    host-side producer hands the updating actor.  Per contiguous layer group:
+    cudaMemcpyAsync of the group's slice on a copy stream -> K3 accumulate
+    into its pages when it lands -> fused sweep of the group, so the PCIe
+    transfer of group k+1 overlaps the update of group k and the step costs
+    about one transfer of the gradient (the reference's fetch/offload are
+    DelayModel sleeps, hiermem/lockfree.py:90-94, 562-569)."""
+    lay = buffer.layout
+    st = buffer._stream(stream)
+    cache = buffer.__dict__.setdefault("_ingest", {})
+    key = ("plan", groups)
+    if key not in cache:
+        cache[key] = layer_groups(lay.numels, groups)
+        cache["staging"] = torch.empty(sum(lay.numels), dtype=buffer._t16, device=buffer.device)
+        cache["copy"] = copy_stream or torch.cuda.Stream(buffer.device)
+        starts = np.cumsum([0] + lay.numels[:-1])
+        cache["starts"] = starts
+    plan, staging, cs, starts = cache[key], cache["staging"], cache["copy"], cache["starts"]
+    src = host_grad.reshape(-1)
+    if src.dtype != buffer._t16 or src.numel() != staging.numel():
+        raise ProtocolError(f"host gradient must be {buffer._t16} with {staging.numel()} elements")
+    L = buffer.num_layers
+    parts = []
+    cs.wait_stream(st)   # the staging slice is free once the previous step consumed it
+    for grp in plan:
+        a, b = int(starts[grp[0]]), int(starts[grp[-1]] + lay.numels[grp[-1]])
+        with torch.cuda.stream(cs):
+            staging[a:b].copy_(src[a:b], non_blocking=True)
+            landed = torch.cuda.Event()
+            landed.record(cs)
+        st.wait_event(landed)
+        gkey = ("acc", tuple(grp), tuple(buffer._gsel[l] for l in grp))
+        if gkey not in cache:
+            rows = []
+            for l in grp:
+                c = lay.seg_chunks(l, "16").copy()
+                c["src_off"] += int(starts[l])
+                c["dst_off"] += buffer._gsel[l] * lay.elems16
+                c["slot"] = buffer._gsel[l] * L + l
+                rows.append(c)
+            cache[gkey] = np.concatenate(rows)
+        chunks = cache[gkey]
+        modes = np.zeros(2 * L, dtype=np.uint8)
+        reset = []
+        for l in grp:
+            f = buffer._gsel[l] * L + l
+            if buffer._pending[l] > 0:
+                modes[f] = 1
+            else:
+                reset.append(f)
+        if reset:
+            idx = buffer._eng.desc.table(np.array(reset, dtype=np.int64)).view(torch.int64)
+            with torch.cuda.stream(st):
+                buffer._flags.index_fill_(0, idx, 0)
+                buffer._sumsq.index_fill_(0, idx, 0)
+        D.check(N.lib().hm_accumulate(
+            D.ptr(staging), buffer._dt, D.ptr(buffer.g16_pool), buffer._dt,
+            D.ptr(buffer._eng.desc.static(chunks)), len(chunks), 0,
+            D.ptr(buffer._eng.desc.table(modes)), D.ptr(buffer._flags), D.ptr(buffer._sumsq),
+            D.sptr(st)))
+        for l in grp:
+            buffer.ledger.messages_accumulated[l] += 1
+            buffer._pending[l] += 1
+            buffer._max_iter[l] = max(buffer._max_iter[l], iteration)
+        parts.append(sweep(buffer, masters, hyper, layers=list(reversed(grp)), stream=st))
+    return _MultiResult(masters, parts)

@@ -237,3 +237,29 @@ def test_three_call_path_equals_sweep(cuda):
     for l in range(len(sizes)):
         np.testing.assert_array_equal(bits(a_ms.p32[l]), bits(b_ms.p32[l]))
         np.testing.assert_array_equal(bits(a_buf.read(l)[1]), bits(b_buf.read(l)[1]))
+
+
+@pytest.mark.parametrize("groups", [1, 3, 8])
+def test_ingest_sweep_equals_accumulate_then_sweep(cuda, groups):
+    """The pipelined host-gradient step (per layer group: H2D -> K3 -> sweep)
+    is bit-identical to accumulate_flat + one sweep, including a rejected layer."""
+    sizes = _layer_sizes()
+    rng = np.random.default_rng(21)
+    params = [rng.normal(0, 0.02, n).astype(np.float32) for n in sizes]
+    tp = [torch.from_numpy(p) for p in params]
+    a_buf, a_ms = LF.ParamBuffer(tp, dtype="bf16", page_bytes=64 * 1024), LF.MasterState(tp, page_bytes=64 * 1024)
+    b_buf, b_ms = LF.ParamBuffer(tp, dtype="bf16", page_bytes=64 * 1024), LF.MasterState(tp, page_bytes=64 * 1024)
+    hyper = LF.AdamHyper(lr=1e-3)
+    for it in range(3):
+        g = rng.normal(0, 1e-2, sum(sizes)).astype(np.float32)
+        if it == 1:
+            g[sizes[0] + 3] = np.inf          # layer 1 rejected this step
+        host = torch.from_numpy(O.to16(g, "bf16").view(np.int16)).view(torch.bfloat16).pin_memory()
+        ra = LF.ingest_sweep(a_buf, a_ms, host, hyper, it, groups=groups).applied()
+        b_buf.accumulate_flat(host.cuda(), it)
+        rb = LF.sweep(b_buf, b_ms, hyper).applied()
+        assert ra == rb and ra[1] == (it != 1)
+    assert a_ms.steps == b_ms.steps
+    for l in range(len(sizes)):
+        assert torch.equal(a_ms.p32[l].view(torch.int32), b_ms.p32[l].view(torch.int32))
+        assert torch.equal(a_buf.layer_view(l).view(torch.int16), b_buf.layer_view(l).view(torch.int16))
