@@ -373,6 +373,9 @@ def main():
     ap.add_argument("--adam-threads", type=int, default=256, choices=[256, 512])
     ap.add_argument("--swap-group-pages", type=int, default=64)
     ap.add_argument("--swap-slots", type=int, default=2)
+    ap.add_argument("--state-tier", default="host", choices=["host", "ssd"],
+                    help="C3: fp32 state in pinned host memory or in a file on the SSD")
+    ap.add_argument("--ssd-dir", default="/tmp", help="directory of the SSD tier's state file")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl != "reference":

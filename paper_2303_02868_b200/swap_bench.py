@@ -1,17 +1,21 @@
-"""bench.py --config c3: the pinned-host page swap tier (GPT-3 13B page pools,
-fp32 master state in host memory, lock-free update order preserved).
+"""bench.py --config c3: GPT-3 13B page pools with the fp32 master state
+off the GPU — pinned host memory (swap tier, ``--state-tier host``) or a
+file on the SSD (``--state-tier ssd``) — lock-free update order preserved.
 
-Host memory of the GPU box bounds the slice: the full 13B model needs
-154 GB of pinned fp32 state (12 B/param), so the default run takes the
+Host memory of the GPU box bounds the host-tier slice: the full 13B model
+needs 154 GB of pinned fp32 state (12 B/param), so the default run takes the
 first ``--c3-layers`` transformer layers plus the embeddings (every layer
 has the same shape, so params/s is size-independent and the full-model step
-time is the per-param time x 12.85e9, stated in the output).  The roofline
-is PCIe: 12 B/param fetched + 12 B/param stored, against pinned
-cudaMemcpyAsync bandwidth measured on the box in the same run.
+time is the per-param time x 12.85e9, stated in the output).  Rooflines:
+PCIe for the host tier (12 B/param fetched + 12 B/param stored, against
+pinned cudaMemcpyAsync bandwidth measured in the same run); the drive for
+the SSD tier (24 B/param of I/O against sequential O_DIRECT read/write
+bandwidth measured on the same file system).
 """
 from __future__ import annotations
 
 import json
+import os
 import time
 
 import torch
@@ -54,11 +58,39 @@ def measure_pcie(device, nbytes=1 << 30, reps=5):
             "bidir_gbs": 2 * nbytes / t_both / 1e9}
 
 
+def measure_drive(path: str, nbytes: int = 2 << 30, block: int = 64 << 20):
+    """Sequential write then read of ``nbytes`` with O_DIRECT (when allowed)
+    from pinned memory, 4 threads, like the tier's own I/O."""
+    from concurrent.futures import ThreadPoolExecutor
+    from .ssd import _open
+    fd, direct = _open(path, True)
+    os.ftruncate(fd, nbytes)
+    bufs = [torch.zeros(block, dtype=torch.uint8, pin_memory=True) for _ in range(4)]
+    views = [memoryview(b.numpy()) for b in bufs]
+
+    def run(write):
+        def one(i):
+            mv = views[i % 4]
+            (os.pwritev if write else os.preadv)(fd, [mv], i * block)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(4) as ex:
+            list(ex.map(one, range(nbytes // block)))
+        if write:
+            os.fsync(fd)
+        return nbytes / (time.perf_counter() - t0) / 1e9
+
+    w = run(True)
+    r = run(False)
+    os.close(fd)
+    os.unlink(path)
+    return {"write_gbs": w, "read_gbs": r, "o_direct": direct,
+            "path": os.path.dirname(os.path.abspath(path))}
+
+
 def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
     from . import lockfree as LF
     from . import workloads as W
     from .layout import PageLayout
-    from .swap import HostMasterState, swap_sweep
     device = torch.device("cuda", 0)
     torch.cuda.set_device(device)
     shape = W.GPTShape(2048, 5120, 20480, args.c3_layers)
@@ -73,8 +105,16 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
               for n in numels]
     buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout)
     t0 = time.perf_counter()
-    hm = HostMasterState(params, page_bytes=page, device=device, layout=layout,
-                         group_pages=args.swap_group_pages, slots=args.swap_slots)
+    ssd_path = None
+    if args.state_tier == "ssd":
+        from .ssd import SSDMasterState, ssd_sweep as sweep_fn
+        ssd_path = os.path.join(args.ssd_dir, f"hm_state_{os.getpid()}.bin")
+        hm = SSDMasterState(params, ssd_path, page_bytes=page, device=device, layout=layout,
+                            group_pages=args.swap_group_pages, slots=max(3, args.swap_slots))
+    else:
+        from .swap import HostMasterState, swap_sweep as sweep_fn
+        hm = HostMasterState(params, page_bytes=page, device=device, layout=layout,
+                             group_pages=args.swap_group_pages, slots=args.swap_slots)
     init_s = time.perf_counter() - t0
     del params
     torch.cuda.empty_cache()
@@ -86,7 +126,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
     for rnd in range(2):
         buf.accumulate_flat(grads, rnd)
         if rnd == 0:
-            swap_sweep(buf, hm, hyper)
+            sweep_fn(buf, hm, hyper)
     L = len(specs)
 
     def rearm():
@@ -95,36 +135,48 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
 
     for _ in range(args.warmup):
         rearm()
-        swap_sweep(buf, hm, hyper)
+        sweep_fn(buf, hm, hyper)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(device)
     with ClockSampler(0) as clk:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        t_wall = time.perf_counter()
         a.record(stream)
         for _ in range(args.steps):
             rearm()
-            swap_sweep(buf, hm, hyper)
+            sweep_fn(buf, hm, hyper)
         b.record(stream)
         torch.cuda.synchronize()
-    ms_step = a.elapsed_time(b) / args.steps
-    pcie = measure_pcie(device)
+        t_wall = time.perf_counter() - t_wall
+    # the SSD sweep blocks on host I/O, so its step time is the wall clock
+    ms_step = (t_wall * 1e3 if args.state_tier == "ssd" else a.elapsed_time(b)) / args.steps
     moved = 24 * P  # 12 B fetched + 12 B stored per param
     achieved = moved / (ms_step / 1e3) / 1e9
+    if args.state_tier == "ssd":
+        hm.close()
+        os.unlink(ssd_path)
+        drive = measure_drive(os.path.join(args.ssd_dir, f"hm_probe_{os.getpid()}.bin"))
+        peak = 1.0 / (0.5 / drive["read_gbs"] + 0.5 / drive["write_gbs"])  # 12 B read + 12 B write
+        roof = {"bound": "ssd", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_kind": "measured sequential pread/pwrite (harmonic mean of read and write) "
+                             "on the same file system", "bytes_per_param": 24, "drive": drive}
+    else:
+        pcie = measure_pcie(device)
+        roof = {"bound": "pcie", "achieved": achieved, "peak": pcie["bidir_gbs"], "unit": "GB/s",
+                "frac": achieved / pcie["bidir_gbs"], "peak_kind": "measured pinned cudaMemcpyAsync "
+                "H2D||D2H on this box", "bytes_per_param": 24, "pcie": pcie}
     line = {
         "metric": metric, "value": P / (ms_step / 1e3), "unit": "params/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": f"c3: GPT-3 13B page pools, first {args.c3_layers} of 40 layers + "
-                               "embeddings; fp32 state in pinned host memory (swap tier)",
+                               f"embeddings; fp32 state on the {args.state_tier} tier",
                    "params": P, "full_model_params": full_params, "layers": L, "page_bytes": page,
                    "pages": layout.used_pages, "group_pages": args.swap_group_pages,
-                   "staging_slots": args.swap_slots, "host_state_gb": 12 * P / 1e9,
-                   "host_init_s": init_s,
-                   "full_model_step_ms_extrapolated": ms_step * full_params / P},
-        "roofline": {"bound": "pcie", "achieved": achieved, "peak": pcie["bidir_gbs"], "unit": "GB/s",
-                     "frac": achieved / pcie["bidir_gbs"], "peak_kind": "measured pinned cudaMemcpyAsync "
-                     "H2D||D2H on this box", "bytes_per_param": 24, "pcie": pcie},
+                   "staging_slots": args.swap_slots, "state_gb": 12 * P / 1e9,
+                   "init_s": init_s, "full_model_step_ms_extrapolated": ms_step * full_params / P},
+        "roofline": roof,
         "clocks": clk.summary(),
         "gpu_launches": args.steps * (1 + hm.num_groups),
     }
