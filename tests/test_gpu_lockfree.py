@@ -253,12 +253,12 @@ def test_ingest_sweep_equals_accumulate_then_sweep(cuda, groups):
     for it in range(3):
         g = rng.normal(0, 1e-2, sum(sizes)).astype(np.float32)
         if it == 1:
-            g[sizes[0] + 3] = np.inf          # layer 1 rejected this step
+            g[sizes[0] + sizes[1] + 3] = np.inf   # an element of layer 2: rejected this step
         host = torch.from_numpy(O.to16(g, "bf16").view(np.int16)).view(torch.bfloat16).pin_memory()
         ra = LF.ingest_sweep(a_buf, a_ms, host, hyper, it, groups=groups).applied()
         b_buf.accumulate_flat(host.cuda(), it)
         rb = LF.sweep(b_buf, b_ms, hyper).applied()
-        assert ra == rb and ra[1] == (it != 1)
+        assert ra == rb and ra[2] == (it != 1)
     assert a_ms.steps == b_ms.steps
     for l in range(len(sizes)):
         assert torch.equal(a_ms.p32[l].view(torch.int32), b_ms.p32[l].view(torch.int32))
