@@ -273,6 +273,11 @@ int hm_copy_runs(const void* src, void* dst, const hm_copy_desc* descs,
 int hm_memcpy_runs(const void* src, void* dst, const hm_copy_desc* descs,
                    int64_t n_descs, int kind, void* stream);
 
+/* A compute slot of modelled duration when executing an Algorithm-1 schedule
+ * (hiermem/scheduler.py:264-403 tasks, durations from hiermem/simengine.py's
+ * timing model): one warp spins on %globaltimer for `ns` nanoseconds. */
+int hm_spin(int64_t ns, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -155,10 +155,51 @@ def toy_sync():
                    "iterations": 25, "loss_curve": ref, "val_loss": sync.val_loss}, f)
 
 
+def schedules():
+    """Algorithm-1 schedules of the reference (scheduler.schedule, phase 2) and
+    their simulate() replay on the measured B200 profile (presets/b200-server.json),
+    for the executor (paper_2303_02868_b200/executor.py) to run with real bytes."""
+    import os
+    os.environ["HIERMEM_PRESET_DIR"] = str(ROOT / "presets")
+    from hiermem import presets
+    from hiermem.scheduler import LayerModel, ShardingModel, peak_memory, schedule
+    from hiermem.simengine import simulate
+    from hiermem.tracer import TimingModel, build_trace
+    prof = presets.hardware_preset("b200-server")
+    out = {}
+    for name, budget in (("tiny-2layer", int(0.012 * 2**30)), ("gpt3-1.7b", 8 * 2**30)):
+        cfg = presets.model_preset(name)
+        inv = footprint.tensor_inventory(cfg)
+        timing = TimingModel(gpu_sec_per_byte=1 / prof.gpu_bytes_per_s,
+                             cpu_sec_per_byte=1 / prof.cpu_bytes_per_s)
+        traces = build_trace(inv, timing)
+        lm = LayerModel.from_inventory(inv, 4 * MIB, cfg.batch_size)
+        sched = schedule(lm, traces, budget, ShardingModel(1, 0))
+        sim = simulate(sched, traces, prof)
+        slot_s = [0.0] * sched.num_slots
+        for e in sim.timeline:
+            if e.operation == "compute":          # task id "it0.compute.s{slot}.l{layer}"
+                slot = int(e.task_id.split(".s")[1].split(".")[0])
+                slot_s[slot] = e.end_s - e.start_s
+        d = sched.to_dict()
+        d["model"].pop("tensors")  # the executor only needs the page numbering
+        out[name] = {"schedule": d, "peak_bytes": peak_memory(sched, traces),
+                     "simulated": {"makespan_s": sim.makespan_s, "busy_s": sim.busy_s,
+                                   "gpu_idle_fraction": sim.gpu_idle_fraction,
+                                   "compute_s_by_slot": slot_s,
+                                   "timeline_compute": [[e.task_id, e.start_s, e.end_s]
+                                                        for e in sim.timeline if e.operation == "compute"]},
+                     "hardware": prof.to_dict()}
+        print(name, len(sched.tasks), "tasks, simulated makespan", sim.makespan_s)
+    with gzip.open(GOLDEN / "schedules.json.gz", "wt") as f:
+        json.dump(out, f)
+
+
 if __name__ == "__main__":
     GOLDEN.mkdir(parents=True, exist_ok=True)
     adam_cases()
     pagetable_random()
     pagetable_configs()
     toy_sync()
+    schedules()
     print("golden fixtures written to", GOLDEN)

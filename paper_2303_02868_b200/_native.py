@@ -87,6 +87,7 @@ SIGNATURES = {
     "hm_reduce_stats": (_INT, [_P, _INT, _P, _I64, _P, _P, _P, _P]),
     "hm_copy_runs": (_INT, [_P, _P, _P, _I64, _P]),
     "hm_memcpy_runs": (_INT, [_P, _P, _P, _I64, _INT, _P]),
+    "hm_spin": (_INT, [_I64, _P]),
 }
 
 _lib = None

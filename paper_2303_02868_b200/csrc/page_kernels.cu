@@ -190,6 +190,17 @@ reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ 
   flush_stats(bad, (float)sq, nonfinite, sumsq, c.slot);
 }
 
+// Occupies one warp of the stream for `ns` nanoseconds of %globaltimer: the
+// stand-in for a compute slot of modelled duration when an Algorithm-1
+// schedule is executed (executor.py); it moves no bytes.
+__global__ void spin_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 // Byte-run copy: one CTA per descriptor; 16-byte vectors once source and
 // destination are co-aligned, 4/2/1-byte granules otherwise.
 __global__ void __launch_bounds__(kThreads)
@@ -352,6 +363,14 @@ int hm_copy_runs(const void* src, void* dst, const hm_copy_desc* descs, int64_t 
   if (n_descs == 0) return HM_OK;
   hm::copy_runs_kernel<<<(unsigned)n_descs, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const char*>(src), static_cast<char*>(dst), descs);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_spin(int64_t ns, void* stream) {
+  if (ns < 0) return hm_set_error(HM_ERR_INVALID, "hm_spin: negative duration");
+  if (ns == 0) return HM_OK;
+  hm::spin_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>((uint64_t)ns);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }
