@@ -94,7 +94,8 @@ class ScheduleExecutor:
         start.record(self.cs)
         self.h2d.wait_event(start)
         self.d2h.wait_event(start)
-        for slot in range(2 * self.L):
+        # triggers run 0..2n: the last backward slot's evictions fire at 2n
+        for slot in range(max(max(by_trigger, default=0), 2 * self.L - 1) + 1):
             for task in by_trigger.get(slot, ()):
                 op, target = task["operation"], task["target"]
                 counts[op] += 1
