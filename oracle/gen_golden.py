@@ -167,11 +167,20 @@ def schedules():
     from hiermem.tracer import TimingModel, build_trace
     prof = presets.hardware_preset("b200-server")
     out = {}
-    for name, budget in (("tiny-2layer", int(0.012 * 2**30)), ("gpt3-1.7b", 8 * 2**30)):
+    cases = [("tiny-2layer", "tiny-2layer", int(0.012 * 2**30), None),
+             ("gpt3-1.7b", "gpt3-1.7b", 8 * 2**30, None)]
+    measured = ROOT / "presets" / "b200-timing-gpt3-1.7b.json"
+    if measured.exists():   # tracer-measured B200 op times (tools/calibrate_timing.py)
+        cases.append(("gpt3-1.7b-measured", "gpt3-1.7b", 8 * 2**30, measured))
+    for key, name, budget, timing_file in cases:
         cfg = presets.model_preset(name)
         inv = footprint.tensor_inventory(cfg)
-        timing = TimingModel(gpu_sec_per_byte=1 / prof.gpu_bytes_per_s,
-                             cpu_sec_per_byte=1 / prof.cpu_bytes_per_s)
+        if timing_file is not None:
+            raw = json.loads(timing_file.read_text())
+            timing = TimingModel.from_dict({"kind": raw["kind"], "table": raw["table"]})
+        else:
+            timing = TimingModel(gpu_sec_per_byte=1 / prof.gpu_bytes_per_s,
+                                 cpu_sec_per_byte=1 / prof.cpu_bytes_per_s)
         traces = build_trace(inv, timing)
         lm = LayerModel.from_inventory(inv, 4 * MIB, cfg.batch_size)
         sched = schedule(lm, traces, budget, ShardingModel(1, 0))
@@ -183,14 +192,15 @@ def schedules():
                 slot_s[slot] = e.end_s - e.start_s
         d = sched.to_dict()
         d["model"].pop("tensors")  # the executor only needs the page numbering
-        out[name] = {"schedule": d, "peak_bytes": peak_memory(sched, traces),
+        out[key] = {"schedule": d, "peak_bytes": peak_memory(sched, traces),
+                    "timing": "measured B200 table" if timing_file else "proportional (bytes / B200 rates)",
                      "simulated": {"makespan_s": sim.makespan_s, "busy_s": sim.busy_s,
                                    "gpu_idle_fraction": sim.gpu_idle_fraction,
                                    "compute_s_by_slot": slot_s,
                                    "timeline_compute": [[e.task_id, e.start_s, e.end_s]
                                                         for e in sim.timeline if e.operation == "compute"]},
                      "hardware": prof.to_dict()}
-        print(name, len(sched.tasks), "tasks, simulated makespan", sim.makespan_s)
+        print(key, len(sched.tasks), "tasks, simulated makespan", sim.makespan_s)
     with gzip.open(GOLDEN / "schedules.json.gz", "wt") as f:
         json.dump(out, f)
 
