@@ -19,6 +19,7 @@ from __future__ import annotations
 import json
 import os
 import statistics
+import sys
 import time
 
 import torch
@@ -62,12 +63,30 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     from .sharding import FusedShardedPageStep, ShardedPageStep, symmetric_alloc
     rank, world, device = _init()
     fused = args.dp_mode != "nccl"
-    specs, page, layout, buf, ms = build_state(args, device, world, rank,
-                                               pool_alloc=symmetric_alloc if fused else None)
+    fallback = None
+    if fused:
+        try:   # symmetric (peer-mapped) pools; every rank must agree on the outcome
+            specs, page, layout, buf, ms = build_state(args, device, world, rank,
+                                                       pool_alloc=symmetric_alloc)
+            dp = FusedShardedPageStep(buf, ms, mode=args.dp_mode)
+            ok = torch.ones(1, device=device)
+        except Exception as e:  # e.g. no peer mapping / multicast on this system
+            fallback = f"{type(e).__name__}: {e}"[:200]
+            ok = torch.zeros(1, device=device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            fallback = fallback or "a peer rank could not map symmetric memory"
+            fused = False
+            buf = ms = dp = None
+            torch.cuda.empty_cache()
+            if rank == 0:
+                print(f"[bench] fused DP path unavailable ({fallback}); using NCCL", file=sys.stderr)
+    if not fused:
+        specs, page, layout, buf, ms = build_state(args, device, world, rank)
+        dp = ShardedPageStep(buf, ms)
     L = len(specs)
     P = sum(layout.numels)
     hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
-    dp = FusedShardedPageStep(buf, ms, mode=args.dp_mode) if fused else ShardedPageStep(buf, ms)
     flat = owned_grad_flat(layout, args.dtype, device, 7 + rank)
     for rnd in range(2):  # fill both gradient page buffers (K3)
         buf.accumulate_flat(flat, rnd)
@@ -143,7 +162,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "page_bytes": page, "pages": layout.used_pages, "bucket_pages_per_rank": layout.K,
                    "buckets": layout.num_buckets, "parallelism": f"dp{world} (page-sharded ZeRO-3)",
                    "l2": "inputs larger than L2",
-                   "dp_mode": args.dp_mode,
+                   "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
                    "step": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
                             "page-Adam(bucket) || AG(bucket)") if not fused else
                            ("barrier -> fused reduce-scatter+check over peer memory -> barrier -> "

@@ -177,7 +177,7 @@ def apply_update(p32, m32, v32, grad, hyper: AdamHyper, step: int, *, stream=Non
     Returns (p32, m32, v32, applied).  Functional like the reference: the
     inputs are never modified; on reject the input objects are returned."""
     numpy_io = not isinstance(p32, torch.Tensor)
-    device = D.require_device(p32.device if not numpy_io else None)
+    device = D.require_device(p32.device if (not numpy_io and p32.is_cuda) else None)
     eng = _Engine.of(device)
     st = D.cur_stream(device, stream)
     shape = _shape(p32)
