@@ -281,6 +281,7 @@ def run_ours_single(args):
         "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": P,
                    "layers": L, "page_bytes": page, "pages": layout.used_pages,
                    "adam_threads": args.adam_threads,
+                   "adam_variant": ["ldg", "tma"][args.adam_variant],
                    "l2": "inputs larger than L2 (28 B/param x params >> 126 MB)",
                    "step": "fused sweep: prologue + page-Adam over all pages (take->update->publish)"},
         "hbm_gbs": achieved,
@@ -371,6 +372,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c3-layers", type=int, default=8, help="C3 slice (host-memory bound)")
     ap.add_argument("--adam-threads", type=int, default=256, choices=[256, 512])
+    ap.add_argument("--adam-variant", type=int, default=0, choices=[0, 1],
+                    help="page-Adam data movement: 0 LDG/STG streaming, 1 TMA bulk-copy pipeline")
     ap.add_argument("--swap-group-pages", type=int, default=64)
     ap.add_argument("--swap-slots", type=int, default=2)
     ap.add_argument("--state-tier", default="host", choices=["host", "ssd"],
@@ -381,6 +384,7 @@ def main():
     if args.impl != "reference":
         from paper_2303_02868_b200 import _native
         _native.check(_native.lib().hm_set_adam_threads(args.adam_threads))
+        _native.check(_native.lib().hm_set_adam_variant(args.adam_variant))
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "c3":

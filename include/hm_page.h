@@ -178,6 +178,11 @@ int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
 /* Tuning knob of the page-Adam main kernel: 256 (default) or 512 threads per
  * 4096-element chunk (2 or 1 granule of 8 elements per thread).  Process-wide. */
 int hm_set_adam_threads(int threads);
+/* Data-movement variant of the page-Adam main pass (same arithmetic, bytes and
+ * results): 0 = LDG/STG streaming kernel (default), 1 = persistent TMA
+ * bulk-copy pipeline (cp.async.bulk + mbarrier, 3 shared-memory stages per SM).
+ * Process-wide. */
+int hm_set_adam_variant(int variant);
 
 /* The two halves of hm_adam_step, for callers that pipeline the main pass
  * (e.g. per all-gather bucket) after ONE prologue over every group: the

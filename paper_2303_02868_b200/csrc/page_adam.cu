@@ -16,9 +16,11 @@
 // The whole-layer reject of lockfree.py:133-134 (+ step rollback :163-164) is
 // decided once per layer by the prologue from the flag that the gradient's
 // producer (hm_accumulate / hm_reduce_stats) fused into its own pass.
+#include "hm_adam.cuh"
 #include "hm_device.cuh"
 #include "hm_dp.cuh"
 #include "hm_error.h"
+#include "hm_tma.h"
 
 namespace hm {
 namespace {
@@ -79,20 +81,6 @@ adam_prologue(const hm_group_launch* __restrict__ groups, int n_groups,
   }
 }
 
-struct AdamScalars {
-  float lr, b1, ob1, b2, ob2, eps, bc1, bc2, gscale;
-};
-
-__device__ __forceinline__ void adam_elem(const AdamScalars& s, float g, float& p, float& m,
-                                          float& v) {
-  g = __fmul_rn(g, s.gscale);  // x * 1.0f == x exactly: identity for parity runs
-  m = __fadd_rn(__fmul_rn(s.b1, m), __fmul_rn(s.ob1, g));
-  v = __fadd_rn(__fmul_rn(s.b2, v), __fmul_rn(s.ob2, __fmul_rn(g, g)));
-  const float mh = __fdiv_rn(m, s.bc1);
-  const float vh = __fdiv_rn(v, s.bc2);
-  const float den = __fadd_rn(__fsqrt_rn(vh), s.eps);
-  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(s.lr, mh), den));
-}
 
 // Publish modes of the 16-bit epilogue: local pool, every peer's pool (P2P
 // stores over NVLink = a fused all-gather), or one NVLS multicast store.
@@ -296,6 +284,9 @@ extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
   hm::AdamFn fn = hm::pick_adam(g_dtype, pdt);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (n_chunks == 0) return HM_OK;
+  if (hm::g_adam_variant == 1)
+    return hm::launch_adam_tma(chunks, n_chunks, groups, rt, g, g_dtype, p32, m32, v32, p16, p16_dtype,
+                               *hyper, static_cast<cudaStream_t>(stream));
   hm::PeerPtrs none{};
   fn<<<(unsigned)n_chunks, hm::g_adam_threads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, groups, rt, g, p32, m32, v32, p16, *hyper, none, nullptr);
