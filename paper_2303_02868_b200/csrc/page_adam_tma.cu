@@ -160,6 +160,7 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
 
   // ---- consumers ----
   const int tid = threadIdx.x;
+  int pending = -1;  // stage whose bulk stores may still be reading shared memory (thread 0)
   for (int it = 0; it < iters; ++it) {
     const int s = it % kStages;
     mbar_wait(&full[s], (it / kStages) & 1);
@@ -200,8 +201,14 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
         if constexpr (kPub)
           bulk_s2g(static_cast<typename Elem<PDT>::T*>(p16) + po, st + L::kOffP16, n * 2);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // TMA done reading the stage
-        mbar_arrive(&empty[s]);
+        // Release the PREVIOUS stage once its stores have read shared memory
+        // (at most this stage's group still reading): the store of chunk i
+        // drains while chunk i+1 is computed.
+        if (pending >= 0) {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          mbar_arrive(&empty[pending]);
+        }
+        pending = s;
       }
     } else {
       for (uint32_t i = tid; i < n; i += kConsumers) {
@@ -216,10 +223,23 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
         if constexpr (kPub) store1<PDT>(p16, po + i, p);
       }
       consumers_sync();
-      if (tid == 0) mbar_arrive(&empty[s]);
+      if (tid == 0) {
+        if (pending >= 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(&empty[pending]);
+          pending = -1;
+        }
+        mbar_arrive(&empty[s]);
+      }
     }
   }
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tid == 0) {
+    if (pending >= 0) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mbar_arrive(&empty[pending]);
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
 }
 
 using TmaFn = void (*)(const hm_adam_chunk*, int, const hm_group_launch*, const hm_group_rt*,
