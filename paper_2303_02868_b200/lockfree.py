@@ -55,6 +55,53 @@ class AdamHyper:
 
 
 @dataclass(frozen=True)
+class DelayModel:
+    """The reference's transfer/compute cost model (hiermem/lockfree.py:81-117),
+    same fields, methods and presets, plus ``"b200"``: the rates this build
+    measured on the GPU box (profiles/r1_raw) — pinned PCIe 55.5 GB/s per
+    direction, the SSD tier's O_DIRECT 4.5 GB/s, and the update itself on
+    the GPU at 28 B/param x 2.41e11 params/s (so ``update_compute_s`` is the
+    page-Adam time instead of a CPU sweep)."""
+
+    pcie_bytes_per_s: float = 32e9
+    ssd_bytes_per_s: float | None = 3.5e9
+    cpu_mem_bytes_per_s: float = 100e9
+    gpu_flops_per_s: float = 1e11
+
+    def fetch_s(self, nbytes: int) -> float:
+        return nbytes / self.pcie_bytes_per_s
+
+    def offload_s(self, nbytes: int) -> float:
+        return nbytes / self.pcie_bytes_per_s
+
+    def state_fetch_s(self, nbytes: int) -> float:
+        rate = self.ssd_bytes_per_s or self.cpu_mem_bytes_per_s
+        return nbytes / rate
+
+    state_store_s = state_fetch_s
+
+    def update_compute_s(self, nbytes_touched: int) -> float:
+        return nbytes_touched / self.cpu_mem_bytes_per_s
+
+    def compute_s(self, flops: float) -> float:
+        return flops / self.gpu_flops_per_s
+
+    @classmethod
+    def preset(cls, name: str) -> "DelayModel":
+        if name == "ssd":
+            return cls()
+        if name == "cpu":
+            return cls(ssd_bytes_per_s=None)
+        if name == "zero":
+            return cls(pcie_bytes_per_s=math.inf, ssd_bytes_per_s=math.inf,
+                       cpu_mem_bytes_per_s=math.inf, gpu_flops_per_s=math.inf)
+        if name == "b200":
+            return cls(pcie_bytes_per_s=55.5e9, ssd_bytes_per_s=4.5e9,
+                       cpu_mem_bytes_per_s=28 * 2.41e11, gpu_flops_per_s=1.37e15)
+        raise ConfigError(f"unknown delay preset {name!r}")
+
+
+@dataclass(frozen=True)
 class GradMessage:
     layer: int
     payload: object  # 16-bit (or f32) gradient, numpy or torch
