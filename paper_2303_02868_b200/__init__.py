@@ -1,7 +1,11 @@
 """B200-native page-granular parameter/optimizer update (Angel-PTM,
 arxiv 2303.02868) — a drop-in for the hot path of the reference ``hiermem``
-package: page pools (hiermem/pagemem.py) and the Adam/buffer update path
-(hiermem/lockfree.py), with the data plane in sm_100a CUDA (libhm_page.so).
+package: page pools (hiermem/pagemem.py), the Adam/buffer update path
+(hiermem/lockfree.py) and page sharding (hiermem/scheduler.py:59-76), with
+the data plane in sm_100a CUDA (libhm_page.so).
+
+The names re-exported here are the reference's (hiermem/__init__.py:8-74)
+for that path; the update-path names load torch lazily on first use.
 """
 from .errors import AllocationError, ConfigError, MoveError, NativeError, ProtocolError
 from .pagemem import (
@@ -23,4 +27,19 @@ from .pagemem import (
 )
 from .workloads import TensorSpec
 
+_LAZY = {
+    "AdamHyper": "lockfree", "DelayModel": "lockfree", "GradMessage": "lockfree",
+    "MasterState": "lockfree", "ParamBuffer": "lockfree", "ConservationLedger": "lockfree",
+    "accumulate_gradient": "lockfree", "apply_update": "lockfree", "publish_params": "lockfree",
+    "sweep": "lockfree", "ingest_sweep": "lockfree", "ShardingModel": "sharding",
+}
+
 __version__ = "0.1.0"
+
+
+def __getattr__(name):
+    mod = _LAZY.get(name)
+    if mod is None:
+        raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
+    import importlib
+    return getattr(importlib.import_module(f".{mod}", __name__), name)
