@@ -98,15 +98,20 @@ def main():
                 else:   # NCCL ring at N>2 / NVLS in-switch reduction: 16-bit rounding bound
                     # Each of the N-1 additions may round by half an ulp of a partial
                     # sum, and every partial sum is bounded by sum_r |g_r|.
+                    # compared with the EXACT (f64) sum: N roundings of at most half an
+                    # ulp of a partial sum bounded by sum_r |g_r|
                     gf, wf = O.from16(got, dtype), O.from16(want, dtype)
                     fin = np.isfinite(wf)
                     u = 2.0 ** -8 if dtype == "bf16" else 2.0 ** -11
                     if fin.any():
-                        absum = np.zeros(s.n, np.float32)
+                        absum = np.zeros(s.n, np.float64)
+                        exact = np.zeros(s.n, np.float64)
                         for r in range(world):
-                            absum += np.abs(O.from16(per_rank[r][l][s.pos:s.pos + s.n], dtype))
-                        bound = (world - 1) * u * absum[fin] + 1e-38
-                        err = np.abs(gf[fin] - wf[fin])
+                            x = O.from16(per_rank[r][l][s.pos:s.pos + s.n], dtype).astype(np.float64)
+                            absum += np.abs(x)
+                            exact += x
+                        bound = world * u * absum[fin] + 1e-38
+                        err = np.abs(gf[fin].astype(np.float64) - exact[fin])
                         worst = float((err / bound).max())
                         stats["max_err_over_bound"] = max(stats.get("max_err_over_bound", 0.0), worst)
                         stats["mismatch"] = stats.get("mismatch", 0) + int((gf[fin] != wf[fin]).sum())
