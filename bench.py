@@ -362,6 +362,9 @@ def main():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
     ap.add_argument("--page-mib", type=int, default=0)
     ap.add_argument("--bucket-pages", type=int, default=32)
+    ap.add_argument("--dp-groups", type=int, default=1,
+                    help="fused DP step: >1 pipelines the reduce-scatter of layer group k+1 with the "
+                         "update + all-gather of group k")
     ap.add_argument("--dp-mode", default="p2p", choices=["nccl", "p2p", "nvls"],
                     help="N>1 collectives: NCCL RS/AG, or fused kernels over NVLink peer memory "
                          "(p2p) / NVSwitch multicast (nvls)")

@@ -87,11 +87,17 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     L = len(specs)
     P = sum(layout.numels)
     hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
+    pipelined = fused and args.dp_groups > 1
+
+    def do_step(**kw):
+        if pipelined:
+            return dp.step_pipelined(hyper, args.dp_groups, **kw)
+        return dp.step(hyper, **kw)
     flat = owned_grad_flat(layout, args.dtype, device, 7 + rank)
     for rnd in range(2):  # fill both gradient page buffers (K3)
         buf.accumulate_flat(flat, rnd)
         if rnd == 0:
-            dp.step(hyper)
+            do_step()
 
     def rearm():
         for l in range(L):
@@ -100,7 +106,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     stream = torch.cuda.current_stream(device)
     for _ in range(args.warmup):
         rearm()
-        dp.step(hyper)
+        do_step()
     torch.cuda.synchronize()
     dist.barrier()
     with ClockSampler(int(os.environ.get("LOCAL_RANK", rank))) as clk:
@@ -110,7 +116,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         t0.record(stream)
         for _ in range(args.steps):
             rearm()
-            dp.step(hyper)
+            do_step()
         t1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -119,7 +125,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     # Component timings (one instrumented step + isolated collectives).
     rearm()
     tm = {}
-    dp.step(hyper, timings=tm)
+    do_step(timings=tm)
     torch.cuda.synchronize()
     mk = tm["_marks"]
     parts = {"rs_ms": mk["start"].elapsed_time(mk["rs"]), "check_ms": mk["rs"].elapsed_time(mk["check"]),
@@ -163,6 +169,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "buckets": layout.num_buckets, "parallelism": f"dp{world} (page-sharded ZeRO-3)",
                    "l2": "inputs larger than L2",
                    "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
+                   "dp_groups": args.dp_groups if pipelined else 1,
                    "step": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
                             "page-Adam(bucket) || AG(bucket)") if not fused else
                            ("barrier -> fused reduce-scatter+check over peer memory -> barrier -> "

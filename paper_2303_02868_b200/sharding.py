@@ -272,6 +272,109 @@ class FusedShardedPageStep:
         import ctypes as C
         return (C.c_uint64 * len(ptrs))(*ptrs)
 
+    def _group_plan(self, groups: int):
+        """Contiguous layer groups with their owned check / adam chunks."""
+        cache = self.__dict__.setdefault("_gplans", {})
+        if groups not in cache:
+            from .lockfree import layer_groups
+            lay = self.layout
+            plan = []
+            for grp in layer_groups(lay.numels, groups):
+                t = tuple(grp)
+                check = lay.pool_chunks(t, "16", owned_only=True).copy()
+                check["slot"] += grp[0]          # flags/sumsq are indexed by global layer
+                plan.append((t, check, lay.adam_chunks(t, "pool", owned_only=True)))
+            cache[groups] = (plan, torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+        return cache[groups]
+
+    def step_pipelined(self, hyper, groups: int = 4, *, stream=None, timings: dict | None = None):
+        """``step`` with the layers cut into contiguous groups and two streams:
+        the reduce-scatter + check of group k+1 runs while group k is updated
+        and all-gathered.  Every group's flags are merged after its own
+        cross-rank barrier, so the whole-layer reject semantics are unchanged.
+        With NVLS the RS leg is outbound-heavy (S out, S/N in per GPU) and the
+        AG leg inbound-heavy (S/N out, S in), so overlapping them moves
+        (1 + 1/N)·S per link direction instead of 2·(N−1)/N·S."""
+        buf, ms, lay = self.buffer, self.masters, self.layout
+        st = buf._stream(stream)
+        L = buf.num_layers
+        if any(p == 0 for p in buf._pending):
+            raise ConfigError("a DP page step needs a gradient for every layer on every rank")
+        gsel, psel = buf._gsel[0], buf._psel[0]
+        if any(x != gsel for x in buf._gsel) or any(x != psel for x in buf._psel):
+            raise ConfigError("DP page step expects all layers in the same page buffers")
+        plan, rs, up = self._group_plan(groups)
+        span_b = lay.elems16 * buf.g16_pool.element_size()
+        span = lay.elems16
+        lib, eng = N.lib(), ms._eng
+        clip = getattr(hyper, "max_norm", 0.0) > 0
+        if clip:
+            raise ConfigError("global grad-norm clipping needs every group's norm first: use step()")
+        marks = {}
+
+        def mark(name, s):
+            if timings is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(s)
+                marks[name] = e
+
+        with torch.cuda.stream(st):
+            mark("start", st)
+            self.flags_local.zero_()
+            self.h_g.barrier(channel=0)                          # every rank's gradients are complete
+        rs.wait_stream(st)
+        up.wait_stream(st)
+        gp = self._arr([p + gsel * span_b for p in self.g_ptrs])
+        mc = self.mc_g + gsel * span_b if self.mc_g else None
+        counts, newest = [0] * L, [0] * L
+        for l in range(L):
+            _, counts[l], newest[l] = buf._hand_over(l, st)
+        bc, bc_len = ms._bias(hyper, range(L))
+        hc = D.hyper_c(hyper)
+        rts = self.__dict__.setdefault("_rts", {})
+        for k, (grp, check, adam) in enumerate(plan):
+            first, n = grp[0], len(grp)
+            with torch.cuda.stream(rs):
+                D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
+                                               D.ptr(eng.desc.static(check)), len(check),
+                                               D.ptr(self.flags_local), None, D.sptr(rs)))
+                self.h_f.barrier(channel=1)                      # group k's flags visible everywhere
+                done = torch.cuda.Event()
+                done.record(rs)
+            up.wait_event(done)
+            with torch.cuda.stream(up):
+                D.check(lib.hm_dp_flags_merge(self._arr([p + 4 * first for p in self.f_ptrs]), None,
+                                              self.n, n, D.ptr(self.flags) + 4 * first, None, D.sptr(up)))
+                rows = np.zeros(n, dtype=N.GROUP_LAUNCH)
+                for i, l in enumerate(grp):
+                    rows[i] = (gsel * span, (psel ^ 1) * span, l, l)
+                dgroups = eng.desc.table(rows)
+                if (k, n) not in rts:
+                    rts[(k, n)] = torch.empty(n * N.GROUP_RT_BYTES, dtype=torch.uint8, device=self.device)
+                rt = rts[(k, n)]
+                D.check(lib.hm_adam_prologue(D.ptr(dgroups), n, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
+                                             D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(self.flags),
+                                             None, 1, D.sptr(up)))
+                D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups),
+                                            D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
+                                            D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
+                                            self.n, self.mc_p if self.mc_p else None, buf._dt, hc,
+                                            D.sptr(up)))
+        mark("rs", rs)
+        st.wait_stream(rs)
+        st.wait_stream(up)
+        with torch.cuda.stream(st):
+            mark("adam", st)
+            self.h_p.barrier(channel=2)                          # published pages landed everywhere
+            mark("ag", st)
+        for l in range(L):
+            buf._psel[l] ^= 1
+            buf._version[l] += 1
+            buf._applied_iter[l] = newest[l]
+        if timings is not None:
+            timings["_marks"] = marks
+        return list(range(L))
+
     def step(self, hyper, *, stream=None, timings: dict | None = None):
         buf, ms, lay = self.buffer, self.masters, self.layout
         st = buf._stream(stream)

@@ -70,7 +70,11 @@ def main():
             t = t.view(torch.bfloat16)
         buf.accumulate_flat(t.to(dev), it)
         gsel = buf._gsel[0]
-        step.step(hyper)
+        groups = int(os.environ.get("DP_GROUPS", "1"))
+        if groups > 1 and mode != "nccl":
+            step.step_pipelined(hyper, groups)
+        else:
+            step.step(hyper)
         # every owner's reduced (post reduce-scatter) pages, gathered so each
         # rank can run the oracle on the exact captured gradient of ALL pages
         gathered = buf.g16_pool[gsel].clone()
