@@ -27,7 +27,7 @@ int g_adam_variant = 0;
 namespace {
 
 constexpr int kStages = 3;
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 16;  // the Adam chain is latency-bound per warp: 16 warps hide it
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kTmaThreads = kConsumers + 32;
 
