@@ -103,35 +103,47 @@ class ClockSampler:
 
 # ---- CPU baseline (oracle port of the reference, bounded sample) ---------------------
 
-def cpu_reference_sample(specs, page_bytes, sample_pages: int, threads: int, dtype: str, reps: int):
-    """Time the reference chain take -> apply_update -> publish cast, restated
+class CpuReferenceSample:
+    """The reference chain take -> apply_update -> publish cast, restated
     op-for-op in numpy (oracle/page_adam.py, pinned to the reference), over
     the first ``sample_pages`` pages' worth of parameters of the workload,
-    fanned out over ``threads`` host threads (numpy ufuncs release the GIL)."""
-    from concurrent.futures import ThreadPoolExecutor
+    fanned out over ``threads`` host threads (numpy ufuncs release the GIL).
+    The synthetic sample is built once; ``run()`` times one pass."""
 
-    from oracle import page_adam as O
-    E = page_bytes // 2
-    n = sample_pages * E
-    p, m, v, g16 = O.synthetic_layer(0, 0, n, dtype, outliers=False)
-    pieces = np.array_split(np.arange(n), threads * 4)
-    bounds = [(int(a[0]), int(a[-1]) + 1) for a in pieces if len(a)]
+    def __init__(self, page_bytes: int, sample_pages: int, threads: int, dtype: str):
+        from concurrent.futures import ThreadPoolExecutor
 
-    def work(b):
-        lo, hi = b
-        g = O.from16(g16[lo:hi], dtype)                                       # take (widen)
-        pp, mm, vv, ok = O.adam_update(p[lo:hi], m[lo:hi], v[lo:hi], g, 1e-3, 0.9, 0.999, 1e-8, 10)
-        O.publish16(pp, dtype)                                              # publish cast
+        from oracle import page_adam as O
+        self.O, self.dtype = O, dtype
+        self.n = sample_pages * (page_bytes // 2)
+        self.p, self.m, self.v, self.g16 = O.synthetic_layer(0, 0, self.n, dtype, outliers=False)
+        pieces = np.array_split(np.arange(self.n), threads * 4)
+        self.bounds = [(int(a[0]), int(a[-1]) + 1) for a in pieces if len(a)]
+        self.pool = ThreadPoolExecutor(max_workers=threads)
+
+    def _work(self, b):
+        O, lo, hi = self.O, b[0], b[1]
+        g = O.from16(self.g16[lo:hi], self.dtype)                                    # take (widen)
+        pp, mm, vv, ok = O.adam_update(self.p[lo:hi], self.m[lo:hi], self.v[lo:hi], g,
+                                       1e-3, 0.9, 0.999, 1e-8, 10)                   # apply_update
+        O.publish16(pp, self.dtype)                                                  # publish cast
         return ok
 
-    best = float("inf")
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(work, bounds))  # warm
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            list(ex.map(work, bounds))
-            best = min(best, time.perf_counter() - t0)
-    return n, best
+    def run(self) -> float:
+        t0 = time.perf_counter()
+        list(self.pool.map(self._work, self.bounds))
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def cpu_reference_sample(specs, page_bytes, sample_pages: int, threads: int, dtype: str, reps: int):
+    s = CpuReferenceSample(page_bytes, sample_pages, threads, dtype)
+    s.run()  # warm
+    best = min(s.run() for _ in range(reps))
+    s.close()
+    return s.n, best
 
 
 def run_reference(args):
@@ -145,12 +157,12 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     E = page // 2
     sample_pages = max(1, min(args.cpu_sample_pages, sum(s.bytes for s in specs) // page))
-    times = []
     n = sample_pages * E
-    for i in range(args.warmup + args.steps):
-        nn, t = cpu_reference_sample(specs, page, sample_pages, threads, args.dtype, reps=1)
-        if i >= args.warmup:
-            times.append(t)
+    sample = CpuReferenceSample(page, sample_pages, threads, args.dtype)
+    for _ in range(args.warmup):
+        sample.run()
+    times = [sample.run() for _ in range(args.steps)]
+    sample.close()
     t = statistics.median(times)
     value = n / t
     line = {
