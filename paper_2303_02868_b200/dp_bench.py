@@ -128,8 +128,14 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     do_step(timings=tm)
     torch.cuda.synchronize()
     mk = tm["_marks"]
-    parts = {"rs_ms": mk["start"].elapsed_time(mk["rs"]), "check_ms": mk["rs"].elapsed_time(mk["check"]),
-             "adam_ms": mk["check"].elapsed_time(mk["adam"]), "ag_tail_ms": mk["adam"].elapsed_time(mk["ag"])}
+    if pipelined:   # reduce of group k+1 overlaps the update of group k: report the spans
+        parts = {"rs_ms": mk["start"].elapsed_time(mk["rs"]), "check_ms": 0.0,
+                 "adam_ms": mk["start"].elapsed_time(mk["adam"]) - mk["start"].elapsed_time(mk["rs"]),
+                 "ag_tail_ms": mk["adam"].elapsed_time(mk["ag"]),
+                 "overlapped_rs_update_ms": mk["start"].elapsed_time(mk["adam"])}
+    else:
+        parts = {"rs_ms": mk["start"].elapsed_time(mk["rs"]), "check_ms": mk["rs"].elapsed_time(mk["check"]),
+                 "adam_ms": mk["check"].elapsed_time(mk["adam"]), "ag_tail_ms": mk["adam"].elapsed_time(mk["ag"])}
     parts = {k: _max_over_ranks(v) for k, v in parts.items()}
     gpool = buf.g16_pool[buf._gsel[0] ^ 1]
     ppool = buf.p16_pool[buf._psel[0]]
@@ -156,7 +162,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     busbw = lambda ms_: pool_bytes / (ms_ / 1e3) * (world - 1) / world / 1e9
     # Sharded page-Adam alone (owned pages) for the HBM roofline.
     owned = layout.owned_numel()
-    adam_ms = _max_over_ranks(parts["adam_ms"])
+    # pipelined: the update kernels overlap the reduce, so only the whole span bounds them
+    adam_ms = parts["overlapped_rs_update_ms"] if pipelined else parts["adam_ms"]
     peak, peak_kind = load_peaks()
     achieved = bytes_per_param * owned / (adam_ms / 1e3) / 1e9 if adam_ms > 0 else None
     line = {
@@ -176,8 +183,10 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                             "flag merge -> prologue -> page-Adam with all-gather epilogue -> barrier")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "peak_kind": peak_kind,
-                     "traffic": None, "kernel": "adam_main on owned pages (instrumented step, "
-                                                "overlapped with AG)", "kernel_ms": adam_ms},
+                     "traffic": None, "kernel": ("adam_main on owned pages (instrumented step, "
+                                                 "overlapped with AG)") if not pipelined else
+                                                ("reduce+update span of the layer-group pipeline "
+                                                 "(adam_main overlapped with RS and AG)"), "kernel_ms": adam_ms},
         "nvlink": {"rs_ms": rs_ms, "ag_ms": ag_ms,
                    "note": ("isolated NCCL collectives" if not fused else
                             "fused kernels: rs = reduce+check kernel; ag = page-Adam with the all-gather "
@@ -187,7 +196,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "pool_bytes": pool_bytes},
         "components_ms": parts,
         "clocks": clk.summary(),
-        "gpu_launches": args.steps * ((2 + layout.num_buckets) if not fused else 4),
+        "gpu_launches": args.steps * ((2 + layout.num_buckets) if not fused else
+                                     4 * (args.dp_groups if pipelined else 1)),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
