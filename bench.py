@@ -377,6 +377,9 @@ def main():
     ap.add_argument("--dp-groups", type=int, default=1,
                     help="fused DP step: >1 pipelines the reduce-scatter of layer group k+1 with the "
                          "update + all-gather of group k")
+    ap.add_argument("--dp-reduce-ctas", type=int, default=0,
+                    help="pipelined DP step: persistent grid of the reduce kernel (0 = one CTA per "
+                         "chunk) so it shares the SMs with the previous group's update")
     ap.add_argument("--dp-mode", default="p2p", choices=["nccl", "p2p", "nvls"],
                     help="N>1 collectives: NCCL RS/AG, or fused kernels over NVLink peer memory "
                          "(p2p) / NVSwitch multicast (nvls)")

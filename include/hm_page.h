@@ -211,6 +211,11 @@ typedef struct hm_seg_chunk hm_seg_chunk;
 int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_pool,
                        void* local_pool, int dtype, const hm_seg_chunk* chunks, int64_t n_chunks,
                        uint32_t* nonfinite, double* sumsq, void* stream);
+/* Grid of hm_dp_reduce_check: 0 (default) = one CTA per chunk; ctas > 0 = a
+ * persistent grid of that many CTAs striding over the chunks, so the reduce
+ * of one layer group can share the SMs with the page-Adam of the previous
+ * group (layer-group pipelined DP step).  Process-wide. */
+int hm_set_dp_reduce_ctas(int ctas);
 /* flags_out[l] = OR_r peer_flags_r[l]; sumsq_out[l] = sum_r peer_sumsq_r[l]
  * (rank order).  Replaces an all-reduce of the per-layer reject flags. */
 int hm_dp_flags_merge(const uint64_t* peer_flags, const uint64_t* peer_sumsq, int n_peers,

@@ -78,16 +78,17 @@ __device__ __forceinline__ void flush(bool bad, float sq, uint32_t* nonfinite, d
     if (nonfinite && b) atomicOr(&nonfinite[slot], 1u);
     if (sumsq && t != 0.f) atomicAdd(&sumsq[slot], (double)t);
   }
+  __syncthreads();   // s_sq / s_bad are reused by the CTA's next chunk
 }
 
-// One CTA per owned chunk; chunk offsets are pool element offsets.
-template <int DT, bool MC>
-__global__ void __launch_bounds__(kThreads)
-reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, PeerPtrs peers, const char* mc,
-                    void* __restrict__ local, uint32_t* __restrict__ nonfinite,
-                    double* __restrict__ sumsq) {
+// One owned chunk; chunk offsets are pool element offsets.  NP = peer count
+// rounded up to 2/4/8, so the in-flight load array is sized to the world.
+template <int DT, bool MC, int NP>
+__device__ __forceinline__ void reduce_chunk(const hm_seg_chunk& c, const PeerPtrs& peers,
+                                             const char* mc, void* __restrict__ local,
+                                             uint32_t* __restrict__ nonfinite,
+                                             double* __restrict__ sumsq) {
   using T = typename Elem<DT>::T;
-  const hm_seg_chunk c = chunks[blockIdx.x];
   const uint64_t off = c.src_off;
   const int tid = threadIdx.x;
   bool bad = false;
@@ -96,7 +97,7 @@ reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, PeerPtrs peers, con
   if (vec) {
     // Every remote load of the thread (granules x peers) is issued before
     // any of them is consumed: NVLink latency (~2 us) needs the depth.
-    uint4 u[kVecPerThread][MC ? 1 : kMaxPeers];
+    uint4 u[kVecPerThread][MC ? 1 : NP];
 #pragma unroll
     for (int k = 0; k < kVecPerThread; ++k) {
       const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
@@ -105,7 +106,7 @@ reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, PeerPtrs peers, con
         u[k][0] = ld_reduce_mc<DT>(mc + (off + e) * sizeof(T));
       } else {
 #pragma unroll
-        for (int r = 0; r < kMaxPeers; ++r)
+        for (int r = 0; r < NP; ++r)
           if (r < peers.n) u[k][r] = ld_peer_u4(reinterpret_cast<const T*>(peers.p[r]) + off + e);
       }
     }
@@ -122,7 +123,7 @@ reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, PeerPtrs peers, con
 #pragma unroll
         for (int j = 0; j < kVec; ++j) acc.v[j] = 0.f;
 #pragma unroll
-        for (int r = 0; r < kMaxPeers; ++r) {
+        for (int r = 0; r < NP; ++r) {
           if (r >= peers.n) break;
           const T* h = reinterpret_cast<const T*>(&u[k][r]);
 #pragma unroll
@@ -153,6 +154,19 @@ reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, PeerPtrs peers, con
   flush(bad, sq, nonfinite, sumsq, c.slot);
 }
 
+// One CTA per chunk (grid = n_chunks), or a persistent grid striding over the
+// chunks: a small resident grid (hm_set_dp_reduce_ctas) keeps the NVLink pipe
+// full from a few SMs and leaves the rest to the page-Adam kernel of the
+// previous layer group running concurrently (FusedShardedPageStep.step_pipelined).
+template <int DT, bool MC, int NP>
+__global__ void __launch_bounds__(kThreads)
+reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, int n_chunks, PeerPtrs peers,
+                    const char* mc, void* __restrict__ local, uint32_t* __restrict__ nonfinite,
+                    double* __restrict__ sumsq) {
+  for (int i = blockIdx.x; i < n_chunks; i += gridDim.x)
+    reduce_chunk<DT, MC, NP>(chunks[i], peers, mc, local, nonfinite, sumsq);
+}
+
 __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, int n,
                                    uint32_t* __restrict__ flags_out, double* __restrict__ sumsq_out) {
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
@@ -167,11 +181,26 @@ __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, in
   }
 }
 
-using RcFn = void (*)(const hm_seg_chunk*, PeerPtrs, const char*, void*, uint32_t*, double*);
+using RcFn = void (*)(const hm_seg_chunk*, int, PeerPtrs, const char*, void*, uint32_t*, double*);
 
-RcFn pick_rc(int dt, bool mc) {
-  if (dt == HM_DT_BF16) return mc ? reduce_check_kernel<HM_DT_BF16, true> : reduce_check_kernel<HM_DT_BF16, false>;
-  if (dt == HM_DT_F16) return mc ? reduce_check_kernel<HM_DT_F16, true> : reduce_check_kernel<HM_DT_F16, false>;
+int g_reduce_ctas = 0;   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
+
+template <int DT, int NP>
+RcFn pick_rc_np(bool mc) {
+  return mc ? reduce_check_kernel<DT, true, 1> : reduce_check_kernel<DT, false, NP>;
+}
+
+template <int DT>
+RcFn pick_rc_dt(bool mc, int n) {
+  if (mc) return reduce_check_kernel<DT, true, 1>;
+  if (n <= 2) return pick_rc_np<DT, 2>(false);
+  if (n <= 4) return pick_rc_np<DT, 4>(false);
+  return pick_rc_np<DT, 8>(false);
+}
+
+RcFn pick_rc(int dt, bool mc, int n) {
+  if (dt == HM_DT_BF16) return pick_rc_dt<HM_DT_BF16>(mc, n);
+  if (dt == HM_DT_F16) return pick_rc_dt<HM_DT_F16>(mc, n);
   return nullptr;
 }
 
@@ -194,14 +223,21 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
                        uint32_t* nonfinite, double* sumsq, void* stream) {
   hm::PeerPtrs peers;
   if (int rc = hm::make_peers(peer_pools, n_peers, &peers)) return rc;
-  hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr);
+  hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, n_peers);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: bad chunk count");
   if (n_chunks == 0) return HM_OK;
-  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      chunks, peers, static_cast<const char*>(mc_pool), local_pool, nonfinite, sumsq);
+  const int64_t grid = hm::g_reduce_ctas > 0 && hm::g_reduce_ctas < n_chunks ? hm::g_reduce_ctas : n_chunks;
+  fn<<<(unsigned)grid, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      chunks, (int)n_chunks, peers, static_cast<const char*>(mc_pool), local_pool, nonfinite, sumsq);
   HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_set_dp_reduce_ctas(int ctas) {
+  if (ctas < 0) return hm_set_error(HM_ERR_INVALID, "hm_set_dp_reduce_ctas: negative grid %d", ctas);
+  hm::g_reduce_ctas = ctas;
   return HM_OK;
 }
 

@@ -91,7 +91,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
 
     def do_step(**kw):
         if pipelined:
-            return dp.step_pipelined(hyper, args.dp_groups, **kw)
+            return dp.step_pipelined(hyper, args.dp_groups, reduce_ctas=args.dp_reduce_ctas, **kw)
         return dp.step(hyper, **kw)
     flat = owned_grad_flat(layout, args.dtype, device, 7 + rank)
     for rnd in range(2):  # fill both gradient page buffers (K3)
@@ -158,8 +158,13 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     else:
         rs_ms = timed(lambda: dp.coll.reduce_scatter(gpool))
         ag_ms = timed(lambda: dp.coll.all_gather(ppool))
+    e2e = run_e2e(args, buf, ms, do_step, flat, layout) if args.e2e_steps > 0 else None
+    # busbw counts the ALGORITHMIC bytes S = 2 B x params; the
+    # padded pool (whole buckets) is larger, but the fused kernels never move
+    # the padding and NCCL's extra bytes are overhead, not useful traffic
     pool_bytes = layout.elems16 * 2
-    busbw = lambda ms_: pool_bytes / (ms_ / 1e3) * (world - 1) / world / 1e9
+    S = 2 * P
+    busbw = lambda ms_: S / (ms_ / 1e3) * (world - 1) / world / 1e9
     # Sharded page-Adam alone (owned pages) for the HBM roofline.
     owned = layout.owned_numel()
     # pipelined: the update kernels overlap the reduce, so only the whole span bounds them
@@ -177,6 +182,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "l2": "inputs larger than L2",
                    "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
                    "dp_groups": args.dp_groups if pipelined else 1,
+                   "dp_reduce_ctas": args.dp_reduce_ctas if pipelined else 0,
                    "step": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
                             "page-Adam(bucket) || AG(bucket)") if not fused else
                            ("barrier -> fused reduce-scatter+check over peer memory -> barrier -> "
@@ -193,13 +199,47 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                             "epilogue (includes the update) + final barrier"), "rs_busbw_gbs": busbw(rs_ms), "ag_busbw_gbs": busbw(ag_ms),
                    "peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                    "nominal_gbs": 900.0, "rs_frac": busbw(rs_ms) / 770.0, "ag_frac": busbw(ag_ms) / 770.0,
-                   "pool_bytes": pool_bytes},
+                   "algorithmic_bytes": S, "pool_bytes_padded": pool_bytes,
+                   "link_bound_ms": 2 * S * (world - 1) / world / 770e9 * 1e3},
         "components_ms": parts,
         "clocks": clk.summary(),
         "gpu_launches": args.steps * ((2 + layout.num_buckets) if not fused else
                                      4 * (args.dp_groups if pipelined else 1)),
     }
+    if e2e:
+        line["e2e"] = e2e
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def run_e2e(args, buf, ms, do_step, flat, layout):
+    """The DP step through the public API with host buffers, per rank: H2D of
+    this rank's whole 16-bit gradient from pinned memory + K3 accumulate
+    (``ParamBuffer.accumulate_flat``), the sharded page step, and a D2H read
+    of the per-layer applied flags.  Time = max over ranks of the wall time
+    between synchronised barriers."""
+    host = flat.cpu().pin_memory()
+    h2d = host.numel() * host.element_size()
+
+    def step(it):
+        buf.accumulate_flat(host, it)      # H2D (non_blocking from pinned) + K3
+        do_step()
+        return ms._applied.cpu()           # D2H of the step's result
+
+    for it in range(2):
+        step(it)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for it in range(args.e2e_steps):
+        step(it)
+    torch.cuda.synchronize()
+    dt = _max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+    P = sum(layout.numels)
+    return {"value": P / dt, "unit": "params/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": 4 * len(layout.numels), "ms_per_step": dt * 1e3,
+            "steps": args.e2e_steps, "h2d_gbs_per_rank": h2d / dt / 1e9,
+            "api": "ParamBuffer.accumulate_flat(pinned host gradient) + sharded page step + "
+                   "applied flags to host, every rank"}

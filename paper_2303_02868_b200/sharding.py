@@ -284,17 +284,26 @@ class FusedShardedPageStep:
                 check = lay.pool_chunks(t, "16", owned_only=True).copy()
                 check["slot"] += grp[0]          # flags/sumsq are indexed by global layer
                 plan.append((t, check, lay.adam_chunks(t, "pool", owned_only=True)))
-            cache[groups] = (plan, torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+            # the reduce stream gets the higher priority: its CTAs are placed
+            # first whenever the update kernel of the previous group frees a slot
+            cache[groups] = (plan, torch.cuda.Stream(self.device, priority=-1),
+                             torch.cuda.Stream(self.device))
         return cache[groups]
 
-    def step_pipelined(self, hyper, groups: int = 4, *, stream=None, timings: dict | None = None):
+    def step_pipelined(self, hyper, groups: int = 4, *, reduce_ctas: int = 0, stream=None,
+                       timings: dict | None = None):
         """``step`` with the layers cut into contiguous groups and two streams:
         the reduce-scatter + check of group k+1 runs while group k is updated
         and all-gathered.  Every group's flags are merged after its own
         cross-rank barrier, so the whole-layer reject semantics are unchanged.
-        With NVLS the RS leg is outbound-heavy (S out, S/N in per GPU) and the
-        AG leg inbound-heavy (S/N out, S in), so overlapping them moves
-        (1 + 1/N)·S per link direction instead of 2·(N−1)/N·S."""
+        Two kernels filling every SM run back to back even on separate
+        streams, so ``reduce_ctas > 0`` launches the reduce as a persistent
+        grid of that many CTAs on a high-priority stream: the link-bound
+        reduce then runs from a few SMs beside the HBM-bound update of the
+        previous group.  With NVLS the RS leg is outbound-heavy (S out, S/N
+        in per GPU) and the AG leg inbound-heavy (S/N out, S in), so
+        overlapping them moves (1 + 1/N)·S per link direction instead of
+        2·(N−1)/N·S."""
         buf, ms, lay = self.buffer, self.masters, self.layout
         st = buf._stream(stream)
         L = buf.num_layers
@@ -332,6 +341,7 @@ class FusedShardedPageStep:
         bc, bc_len = ms._bias(hyper, range(L))
         hc = D.hyper_c(hyper)
         rts = self.__dict__.setdefault("_rts", {})
+        D.check(lib.hm_set_dp_reduce_ctas(int(reduce_ctas)))   # persistent reduce grid (0 = per chunk)
         for k, (grp, check, adam) in enumerate(plan):
             first, n = grp[0], len(grp)
             with torch.cuda.stream(rs):
@@ -360,6 +370,7 @@ class FusedShardedPageStep:
                                             D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
                                             self.n, self.mc_p if self.mc_p else None, buf._dt, hc,
                                             D.sptr(up)))
+        D.check(lib.hm_set_dp_reduce_ctas(0))
         mark("rs", rs)
         st.wait_stream(rs)
         st.wait_stream(up)
