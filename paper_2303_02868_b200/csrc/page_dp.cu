@@ -81,90 +81,114 @@ __device__ __forceinline__ void flush(bool bad, float sq, uint32_t* nonfinite, d
   __syncthreads();   // s_sq / s_bad are reused by the CTA's next chunk
 }
 
-// One owned chunk; chunk offsets are pool element offsets.  NP = peer count
-// rounded up to 2/4/8, so the in-flight load array is sized to the world.
-template <int DT, bool MC, int NP>
-__device__ __forceinline__ void reduce_chunk(const hm_seg_chunk& c, const PeerPtrs& peers,
-                                             const char* mc, void* __restrict__ local,
-                                             uint32_t* __restrict__ nonfinite,
-                                             double* __restrict__ sumsq) {
+// M owned chunks per CTA pass; chunk offsets are pool element offsets.
+// NP = peer count rounded up to 2/4/8, so the in-flight load array is sized
+// to the world.  Every remote load of the pass (chunks x granules x peers) is
+// issued before any of them is consumed: NVLink latency (~2 us) needs the
+// depth, and M > 1 deepens it for a small persistent grid.
+template <int DT, bool MC, int NP, int M>
+__device__ __forceinline__ void reduce_chunks(const hm_seg_chunk* __restrict__ chunks, int first,
+                                              int n_chunks, const PeerPtrs& peers, const char* mc,
+                                              void* __restrict__ local,
+                                              uint32_t* __restrict__ nonfinite,
+                                              double* __restrict__ sumsq) {
   using T = typename Elem<DT>::T;
-  const uint64_t off = c.src_off;
   const int tid = threadIdx.x;
-  bool bad = false;
-  float sq = 0.f;
-  const bool vec = ((off | (uint64_t)c.n) & (kVec - 1)) == 0;
-  if (vec) {
-    // Every remote load of the thread (granules x peers) is issued before
-    // any of them is consumed: NVLink latency (~2 us) needs the depth.
-    uint4 u[kVecPerThread][MC ? 1 : NP];
+  hm_seg_chunk c[M];
+  bool vec[M];
+  uint4 u[M][kVecPerThread][MC ? 1 : NP];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    if (first + m < n_chunks) {
+      c[m] = chunks[first + m];
+    } else {
+      c[m].src_off = 0;
+      c[m].n = 0;
+      c[m].slot = 0;
+    }
+    vec[m] = ((c[m].src_off | (uint64_t)c[m].n) & (kVec - 1)) == 0;
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    if (!vec[m]) continue;
 #pragma unroll
     for (int k = 0; k < kVecPerThread; ++k) {
       const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
-      if (e >= c.n) continue;
+      if (e >= c[m].n) continue;
       if constexpr (MC) {
-        u[k][0] = ld_reduce_mc<DT>(mc + (off + e) * sizeof(T));
+        u[m][k][0] = ld_reduce_mc<DT>(mc + (c[m].src_off + e) * sizeof(T));
       } else {
 #pragma unroll
         for (int r = 0; r < NP; ++r)
-          if (r < peers.n) u[k][r] = ld_peer_u4(reinterpret_cast<const T*>(peers.p[r]) + off + e);
+          if (r < peers.n)
+            u[m][k][r] = ld_peer_u4(reinterpret_cast<const T*>(peers.p[r]) + c[m].src_off + e);
       }
-    }
-#pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
-      if (e >= c.n) continue;
-      F8 acc;
-      if constexpr (MC) {
-        const T* h = reinterpret_cast<const T*>(&u[k][0]);
-#pragma unroll
-        for (int j = 0; j < kVec; ++j) acc.v[j] = Elem<DT>::widen(h[j]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < kVec; ++j) acc.v[j] = 0.f;
-#pragma unroll
-        for (int r = 0; r < NP; ++r) {
-          if (r >= peers.n) break;
-          const T* h = reinterpret_cast<const T*>(&u[k][r]);
-#pragma unroll
-          for (int j = 0; j < kVec; ++j) acc.v[j] = __fadd_rn(acc.v[j], Elem<DT>::widen(h[j]));
-        }
-      }
-      F8 o;
-#pragma unroll
-      for (int j = 0; j < kVec; ++j) {
-        const float r = Elem<DT>::widen(Elem<DT>::narrow(acc.v[j]));
-        bad |= !is_finite(r);
-        sq += __fmul_rn(r, r);
-        o.v[j] = r;
-      }
-      store8<DT>(local, off + e, o);
-    }
-  } else {
-    for (uint32_t i = tid; i < c.n; i += kThreads) {
-      float a = 0.f;
-      for (int r = 0; r < peers.n; ++r)
-        a = __fadd_rn(a, Elem<DT>::widen(reinterpret_cast<const T*>(peers.p[r])[off + i]));
-      const float r = Elem<DT>::widen(Elem<DT>::narrow(a));
-      bad |= !is_finite(r);
-      sq += __fmul_rn(r, r);
-      store1<DT>(local, off + i, r);
     }
   }
-  flush(bad, sq, nonfinite, sumsq, c.slot);
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    if (c[m].n == 0) continue;   // uniform over the CTA
+    const uint64_t off = c[m].src_off;
+    bool bad = false;
+    float sq = 0.f;
+    if (vec[m]) {
+#pragma unroll
+      for (int k = 0; k < kVecPerThread; ++k) {
+        const uint32_t e = (uint32_t)(k * kThreads + tid) * kVec;
+        if (e >= c[m].n) continue;
+        F8 acc;
+        if constexpr (MC) {
+          const T* h = reinterpret_cast<const T*>(&u[m][k][0]);
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) acc.v[j] = Elem<DT>::widen(h[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) acc.v[j] = 0.f;
+#pragma unroll
+          for (int r = 0; r < NP; ++r) {
+            if (r >= peers.n) break;
+            const T* h = reinterpret_cast<const T*>(&u[m][k][r]);
+#pragma unroll
+            for (int j = 0; j < kVec; ++j) acc.v[j] = __fadd_rn(acc.v[j], Elem<DT>::widen(h[j]));
+          }
+        }
+        F8 o;
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) {
+          const float r = Elem<DT>::widen(Elem<DT>::narrow(acc.v[j]));
+          bad |= !is_finite(r);
+          sq += __fmul_rn(r, r);
+          o.v[j] = r;
+        }
+        store8<DT>(local, off + e, o);
+      }
+    } else {
+      for (uint32_t i = tid; i < c[m].n; i += kThreads) {
+        float a = 0.f;
+        for (int r = 0; r < peers.n; ++r)
+          a = __fadd_rn(a, Elem<DT>::widen(reinterpret_cast<const T*>(peers.p[r])[off + i]));
+        const float r = Elem<DT>::widen(Elem<DT>::narrow(a));
+        bad |= !is_finite(r);
+        sq += __fmul_rn(r, r);
+        store1<DT>(local, off + i, r);
+      }
+    }
+    flush(bad, sq, nonfinite, sumsq, c[m].slot);
+  }
 }
 
-// One CTA per chunk (grid = n_chunks), or a persistent grid striding over the
-// chunks: a small resident grid (hm_set_dp_reduce_ctas) keeps the NVLink pipe
-// full from a few SMs and leaves the rest to the page-Adam kernel of the
-// previous layer group running concurrently (FusedShardedPageStep.step_pipelined).
-template <int DT, bool MC, int NP>
+// One CTA per chunk (M = 1, grid = n_chunks), or a persistent grid striding
+// over the chunks M at a time: a small resident grid (hm_set_dp_reduce_ctas)
+// keeps the NVLink pipe full from a few SMs and leaves the rest to the
+// page-Adam kernel of the previous layer group running concurrently
+// (FusedShardedPageStep.step_pipelined).
+template <int DT, bool MC, int NP, int M>
 __global__ void __launch_bounds__(kThreads)
 reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, int n_chunks, PeerPtrs peers,
                     const char* mc, void* __restrict__ local, uint32_t* __restrict__ nonfinite,
                     double* __restrict__ sumsq) {
-  for (int i = blockIdx.x; i < n_chunks; i += gridDim.x)
-    reduce_chunk<DT, MC, NP>(chunks[i], peers, mc, local, nonfinite, sumsq);
+  for (int i = blockIdx.x * M; i < n_chunks; i += gridDim.x * M)
+    reduce_chunks<DT, MC, NP, M>(chunks, i, n_chunks, peers, mc, local, nonfinite, sumsq);
 }
 
 __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, int n,
@@ -185,22 +209,29 @@ using RcFn = void (*)(const hm_seg_chunk*, int, PeerPtrs, const char*, void*, ui
 
 int g_reduce_ctas = 0;   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
 
+// Chunks per pass of the persistent grid: as deep as the registers allow.
+template <int NP>
+constexpr int persistent_depth() { return NP <= 2 ? 4 : NP <= 4 ? 2 : 1; }
+
 template <int DT, int NP>
-RcFn pick_rc_np(bool mc) {
-  return mc ? reduce_check_kernel<DT, true, 1> : reduce_check_kernel<DT, false, NP>;
+RcFn pick_rc_np(bool persistent) {
+  return persistent ? reduce_check_kernel<DT, false, NP, persistent_depth<NP>()>
+                    : reduce_check_kernel<DT, false, NP, 1>;
 }
 
 template <int DT>
-RcFn pick_rc_dt(bool mc, int n) {
-  if (mc) return reduce_check_kernel<DT, true, 1>;
-  if (n <= 2) return pick_rc_np<DT, 2>(false);
-  if (n <= 4) return pick_rc_np<DT, 4>(false);
-  return pick_rc_np<DT, 8>(false);
+RcFn pick_rc_dt(bool mc, int n, bool persistent) {
+  if (mc) return reduce_check_kernel<DT, true, 1, 1>;   // one in-switch load per granule
+  if (n <= 2) return pick_rc_np<DT, 2>(persistent);
+  if (n <= 4) return pick_rc_np<DT, 4>(persistent);
+  return pick_rc_np<DT, 8>(persistent);
 }
 
-RcFn pick_rc(int dt, bool mc, int n) {
-  if (dt == HM_DT_BF16) return pick_rc_dt<HM_DT_BF16>(mc, n);
-  if (dt == HM_DT_F16) return pick_rc_dt<HM_DT_F16>(mc, n);
+RcFn pick_rc(int dt, bool mc, int n, bool persistent, int* depth) {
+  *depth = !persistent || mc ? 1 : n <= 2 ? persistent_depth<2>() : n <= 4 ? persistent_depth<4>()
+                                                                              : persistent_depth<8>();
+  if (dt == HM_DT_BF16) return pick_rc_dt<HM_DT_BF16>(mc, n, persistent);
+  if (dt == HM_DT_F16) return pick_rc_dt<HM_DT_F16>(mc, n, persistent);
   return nullptr;
 }
 
@@ -223,12 +254,15 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
                        uint32_t* nonfinite, double* sumsq, void* stream) {
   hm::PeerPtrs peers;
   if (int rc = hm::make_peers(peer_pools, n_peers, &peers)) return rc;
-  hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, n_peers);
-  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: bad chunk count");
   if (n_chunks == 0) return HM_OK;
-  const int64_t grid = hm::g_reduce_ctas > 0 && hm::g_reduce_ctas < n_chunks ? hm::g_reduce_ctas : n_chunks;
+  const bool persistent = hm::g_reduce_ctas > 0;
+  int depth = 1;
+  hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, n_peers, persistent, &depth);
+  if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
+  const int64_t passes = (n_chunks + depth - 1) / depth;
+  const int64_t grid = persistent && hm::g_reduce_ctas < passes ? hm::g_reduce_ctas : passes;
   fn<<<(unsigned)grid, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, (int)n_chunks, peers, static_cast<const char*>(mc_pool), local_pool, nonfinite, sumsq);
   HM_CUDA_CHECK_LAUNCH();

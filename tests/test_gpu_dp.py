@@ -14,16 +14,18 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("bucket,dtype,mode,groups", [(1, "bf16", "nccl", 1), (2, "bf16", "nccl", 1),
-                                                      (2, "fp16", "nccl", 1), (2, "bf16", "p2p", 1),
-                                                      (2, "fp16", "p2p", 1), (3, "bf16", "nvls", 1),
-                                                      (2, "bf16", "p2p", 3), (2, "bf16", "nvls", 4)])
-def test_dp_step_matches_oracle(bucket, dtype, mode, groups):
+@pytest.mark.parametrize("bucket,dtype,mode,groups,ctas", [
+    (1, "bf16", "nccl", 1, 0), (2, "bf16", "nccl", 1, 0), (2, "fp16", "nccl", 1, 0),
+    (2, "bf16", "p2p", 1, 0), (2, "fp16", "p2p", 1, 0), (3, "bf16", "nvls", 1, 0),
+    (2, "bf16", "p2p", 3, 0), (2, "bf16", "nvls", 4, 0),
+    (2, "bf16", "p2p", 3, 5)])   # persistent reduce grid: 5 CTAs striding over the chunks
+def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = 4 if n >= 4 else 2
-    env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype, DP_MODE=mode, DP_GROUPS=str(groups))
+    env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype, DP_MODE=mode, DP_GROUPS=str(groups),
+               DP_REDUCE_CTAS=str(ctas))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29611", str(ROOT / "tests" / "dp_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--reduce-ctas", type=int, nargs="*", default=[])
     args = ap.parse_args()
     n = min(args.gpus, torch.cuda.device_count())
     if n < 2:
@@ -128,6 +129,13 @@ def main():
         up_ms.append(phase(upd))
     lay = ranks[0]["lay"]
     S = 2 * sum(lay.numels)   # algorithmic bytes: the padding of the pool never moves
+    # reduce alone on a persistent grid of C CTAs (the pipelined step's knob)
+    rs_by_ctas = {}
+    for ctas in args.reduce_ctas:
+        D.check(lib.hm_set_dp_reduce_ctas(ctas))
+        phase(rs)
+        rs_by_ctas[ctas] = float(np.median([phase(rs) for _ in range(3)]))
+    D.check(lib.hm_set_dp_reduce_ctas(0))
 
     # Copy-engine reference for the same exchange: every GPU pulls S/N bytes
     # from every peer at once (cudaMemcpyAsync peer copies, one stream per peer).
@@ -168,6 +176,7 @@ def main():
         "adam_ag_ms": t_up, "ag_busbw_gbs": bus(t_up), "ag_frac_770": bus(t_up) / 770.0,
         "adam_hbm_gbs": 28 * owned / (t_up / 1e3) / 1e9,
         "ce_pull_ms": ce_ms, "ce_pull_busbw_gbs": bus(ce_ms),
+        "reduce_ms_by_persistent_ctas": rs_by_ctas,
         "rs_nvlink_bytes_in_per_gpu": S * (n - 1) / n, "ag_nvlink_bytes_out_per_gpu": S * (n - 1) / n,
     }))
 
