@@ -374,9 +374,11 @@ def main():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
     ap.add_argument("--page-mib", type=int, default=0)
     ap.add_argument("--bucket-pages", type=int, default=32)
-    ap.add_argument("--dp-groups", type=int, default=1,
+    ap.add_argument("--dp-groups", type=int, default=-1,
                     help="fused DP step: >1 pipelines the reduce-scatter of layer group k+1 with the "
-                         "update + all-gather of group k")
+                         "update + all-gather of group k; -1 = auto (8 groups with a 128-CTA reduce "
+                         "grid at N=2, where the update is HBM-bound; 1 at N>=4, where the whole "
+                         "step is NVLink-bound — profiles/r1_dp_c2.md)")
     ap.add_argument("--dp-reduce-ctas", type=int, default=0,
                     help="pipelined DP step: persistent grid of the reduce kernel (0 = one CTA per "
                          "chunk) so it shares the SMs with the previous group's update")

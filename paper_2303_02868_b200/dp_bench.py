@@ -87,6 +87,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     L = len(specs)
     P = sum(layout.numels)
     hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
+    if args.dp_groups < 0:   # auto: measured policy (profiles/r1_dp_c2.md)
+        args.dp_groups, args.dp_reduce_ctas = (8, 128) if world == 2 else (1, 0)
     pipelined = fused and args.dp_groups > 1
 
     def do_step(**kw):
