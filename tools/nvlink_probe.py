@@ -48,6 +48,8 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--reduce-ctas", type=int, nargs="*", default=[])
+    ap.add_argument("--solo", action="store_true",
+                    help="only GPU 0 launches (clean ncu counters: no peer traffic into GPU 0)")
     args = ap.parse_args()
     n = min(args.gpus, torch.cuda.device_count())
     if n < 2:
@@ -92,7 +94,7 @@ def main():
 
     def phase(fn):
         evs = []
-        for x in ranks:
+        for x in (ranks[:1] if args.solo else ranks):
             with torch.cuda.device(x["dev"]), torch.cuda.stream(x["stream"]):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(x["stream"])
