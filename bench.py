@@ -379,6 +379,9 @@ def main():
                          "update + all-gather of group k; -1 = auto (8 groups with a 128-CTA reduce "
                          "grid at N=2, where the update is HBM-bound; 1 at N>=4, where the whole "
                          "step is NVLink-bound — profiles/r1_dp_c2.md)")
+    ap.add_argument("--ag-publish", type=int, default=0, choices=[0, 1, 2],
+                    help="fused DP all-gather epilogue: 0 per-thread peer stores, 1 per-CTA bulk "
+                         "copies (cp.async.bulk), 2 bulk + wait for remote completion")
     ap.add_argument("--dp-reduce-ctas", type=int, default=0,
                     help="pipelined DP step: persistent grid of the reduce kernel (0 = one CTA per "
                          "chunk) so it shares the SMs with the previous group's update")

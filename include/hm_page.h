@@ -228,6 +228,13 @@ int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_grou
                     float* p32, float* m32, float* v32,
                     const uint64_t* peer_p16, int n_peers, void* mc_p16, int p16_dtype,
                     const hm_adam_hyper* hyper, void* stream);
+/* Publish epilogue of hm_adam_main_ag over P2P (no multicast): 0 = every
+ * thread stores its 16 B granules into every peer (default); 1 = the CTA
+ * stages its 16-bit chunk in shared memory and one thread pushes it to every
+ * peer with cp.async.bulk; 2 = as 1, the CTA also waits for the remote
+ * writes to complete before it retires.  Same bytes, same results.
+ * Process-wide. */
+int hm_set_ag_publish(int mode);
 
 /* Elementwise segment chunk used by accumulate / cast / reduce. */
 typedef struct hm_seg_chunk {

@@ -84,7 +84,15 @@ adam_prologue(const hm_group_launch* __restrict__ groups, int n_groups,
 
 // Publish modes of the 16-bit epilogue: local pool, every peer's pool (P2P
 // stores over NVLink = a fused all-gather), or one NVLS multicast store.
-constexpr int kPubLocal = 0, kPubPeers = 1, kPubMulticast = 2;
+// kPubPeersBulk: the CTA stages its published chunk in shared memory and one
+// thread pushes it to every peer with cp.async.bulk (one 8 KB bulk copy per
+// peer instead of 512 per-thread 16 B stores; the stores no longer occupy the
+// warps that stream the HBM state).
+constexpr int kPubLocal = 0, kPubPeers = 1, kPubMulticast = 2, kPubPeersBulk = 3,
+              kPubPeersBulkWait = 4;   // bulk + wait for the remote writes before the CTA retires
+template <int PUB>
+constexpr bool is_bulk() { return PUB == kPubPeersBulk || PUB == kPubPeersBulkWait; }
+int g_ag_publish = 0;   // hm_set_ag_publish: 0 per-thread stores; 1 bulk; 2 bulk + full wait
 
 template <int PDT, int PUB>
 __device__ __forceinline__ void publish8(void* p16, const PeerPtrs& peers, char* mc, uint64_t po,
@@ -97,7 +105,7 @@ __device__ __forceinline__ void publish8(void* p16, const PeerPtrs& peers, char*
     T* h = reinterpret_cast<T*>(&u);
 #pragma unroll
     for (int i = 0; i < 8; ++i) h[i] = Elem<PDT>::narrow(v.v[i]);
-    if constexpr (PUB == kPubPeers) {
+    if constexpr (PUB == kPubPeers || is_bulk<PUB>()) {
 #pragma unroll
       for (int r = 0; r < kMaxPeers; ++r)
         if (r < peers.n) st_stream_u4(reinterpret_cast<T*>(peers.p[r]) + po, u);
@@ -136,6 +144,7 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
   const uint32_t n = c.n;
   const int tid = threadIdx.x;
   constexpr bool kPub = PDT != 0;
+  __shared__ __align__(128) uint4 s_pub[is_bulk<PUB>() ? kChunk / kVec : 1];
 
   if (!r.apply) {
     // Rejected layer: state untouched; still publish the unchanged masters.
@@ -188,7 +197,34 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
       store8<HM_DT_F32>(p32, so + e, pv[k]);
       store8<HM_DT_F32>(m32, so + e, mv[k]);
       store8<HM_DT_F32>(v32, so + e, vv[k]);
-      if constexpr (kPub) publish8<PDT, PUB>(p16, peers, mc, po + e, pv[k]);
+      if constexpr (is_bulk<PUB>()) {
+        using T = typename Elem<PDT>::T;
+        uint4 u;
+        T* h = reinterpret_cast<T*>(&u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) h[i] = Elem<PDT>::narrow(pv[k].v[i]);
+        s_pub[e / kVec] = u;
+      } else if constexpr (kPub) {
+        publish8<PDT, PUB>(p16, peers, mc, po + e, pv[k]);
+      }
+    }
+    if constexpr (is_bulk<PUB>()) {
+      __syncthreads();
+      if (tid == 0) {
+        using T = typename Elem<PDT>::T;
+        const uint32_t src = (uint32_t)__cvta_generic_to_shared(s_pub);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int r = 0; r < peers.n; ++r) {
+          T* dst = reinterpret_cast<T*>(peers.p[r]) + po;
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       ::"l"(dst), "r"(src), "r"(n * (uint32_t)sizeof(T)) : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if constexpr (PUB == kPubPeersBulkWait)
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        else
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
     }
   } else {
     for (uint32_t i = tid; i < n; i += NT) {
@@ -206,14 +242,22 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
 using AdamFn = void (*)(const hm_adam_chunk*, const hm_group_launch*, const hm_group_rt*,
                         const void*, float*, float*, float*, void*, hm_adam_hyper, PeerPtrs, char*);
 
+template <int DT>
+AdamFn pick_adam_ag_dt(int pub) {
+  switch (pub) {
+    case kPubPeers: return adam_main<DT, DT, kPubPeers>;
+    case kPubMulticast: return adam_main<DT, DT, kPubMulticast>;
+    case kPubPeersBulk: return adam_main<DT, DT, kPubPeersBulk>;
+    case kPubPeersBulkWait: return adam_main<DT, DT, kPubPeersBulkWait>;
+  }
+  return nullptr;
+}
+
 AdamFn pick_adam_ag(int gdt, int pdt, int pub) {
-  if (gdt != HM_DT_BF16 && gdt != HM_DT_F16) return nullptr;
   if (pdt != gdt) return nullptr;
-  if (gdt == HM_DT_BF16)
-    return pub == kPubPeers ? adam_main<HM_DT_BF16, HM_DT_BF16, kPubPeers>
-                            : adam_main<HM_DT_BF16, HM_DT_BF16, kPubMulticast>;
-  return pub == kPubPeers ? adam_main<HM_DT_F16, HM_DT_F16, kPubPeers>
-                          : adam_main<HM_DT_F16, HM_DT_F16, kPubMulticast>;
+  if (gdt == HM_DT_BF16) return pick_adam_ag_dt<HM_DT_BF16>(pub);
+  if (gdt == HM_DT_F16) return pick_adam_ag_dt<HM_DT_F16>(pub);
+  return nullptr;
 }
 
 int g_adam_threads = kThreads;  // tuning knob: hm_set_adam_threads
@@ -301,6 +345,13 @@ extern "C" int hm_set_adam_threads(int threads) {
   return HM_OK;
 }
 
+extern "C" int hm_set_ag_publish(int mode) {
+  if (mode < 0 || mode > 2)
+    return hm_set_error(HM_ERR_INVALID, "hm_set_ag_publish: 0, 1 or 2, got %d", mode);
+  hm::g_ag_publish = mode;
+  return HM_OK;
+}
+
 extern "C" int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks,
                                const hm_group_launch* groups, const hm_group_rt* rt, const void* g,
                                int g_dtype, float* p32, float* m32, float* v32,
@@ -309,7 +360,9 @@ extern "C" int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks,
   if (!hyper || !rt) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: missing hyper/rt");
   hm::PeerPtrs peers;
   if (int rc = hm::make_peers(peer_p16, n_peers, &peers)) return rc;
-  const int pub = mc_p16 ? hm::kPubMulticast : hm::kPubPeers;
+  const int pub = mc_p16 ? hm::kPubMulticast
+                 : hm::g_ag_publish == 1 ? hm::kPubPeersBulk
+                 : hm::g_ag_publish == 2 ? hm::kPubPeersBulkWait : hm::kPubPeers;
   hm::AdamFn fn = hm::pick_adam_ag(g_dtype, p16_dtype, pub);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: unsupported dtypes g=%d p16=%d", g_dtype, p16_dtype);
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)

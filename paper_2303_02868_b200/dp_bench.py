@@ -87,6 +87,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     L = len(specs)
     P = sum(layout.numels)
     hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
+    from . import _native as NL
+    NL.check(NL.lib().hm_set_ag_publish(args.ag_publish))
     if args.dp_groups < 0:   # auto: measured policy (profiles/r1_dp_c2.md)
         args.dp_groups, args.dp_reduce_ctas = (8, 128) if world == 2 else (1, 0)
     pipelined = fused and args.dp_groups > 1
@@ -185,6 +187,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
                    "dp_groups": args.dp_groups if pipelined else 1,
                    "dp_reduce_ctas": args.dp_reduce_ctas if pipelined else 0,
+                   "ag_publish": ["per-thread stores", "bulk", "bulk+wait"][args.ag_publish],
                    "step": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
                             "page-Adam(bucket) || AG(bucket)") if not fused else
                            ("barrier -> fused reduce-scatter+check over peer memory -> barrier -> "

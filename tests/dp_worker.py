@@ -42,6 +42,8 @@ def main():
                          device=dev, layout=lay, pool_alloc=None if mode == "nccl" else symmetric_alloc)
     ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay)
     step = ShardedPageStep(buf, ms) if mode == "nccl" else FusedShardedPageStep(buf, ms, mode=mode)
+    from paper_2303_02868_b200 import _native as NL
+    NL.check(NL.lib().hm_set_ag_publish(int(os.environ.get("DP_AG_PUBLISH", "0"))))
     if mode == "nvls" and step is None:
         sys.exit(0)
     from paper_2303_02868_b200.sharding import PageCollectives

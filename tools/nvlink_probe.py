@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--reduce-ctas", type=int, nargs="*", default=[])
+    ap.add_argument("--ag-publish", type=int, nargs="*", default=[])
     ap.add_argument("--solo", action="store_true",
                     help="only GPU 0 launches (clean ncu counters: no peer traffic into GPU 0)")
     args = ap.parse_args()
@@ -131,6 +132,13 @@ def main():
         up_ms.append(phase(upd))
     lay = ranks[0]["lay"]
     S = 2 * sum(lay.numels)   # algorithmic bytes: the padding of the pool never moves
+    # update + AG with the bulk-copy publish epilogues
+    upd_by_publish = {}
+    for mode in args.ag_publish:
+        D.check(lib.hm_set_ag_publish(mode))
+        phase(upd)
+        upd_by_publish[mode] = float(np.median([phase(upd) for _ in range(3)]))
+    D.check(lib.hm_set_ag_publish(0))
     # reduce alone on a persistent grid of C CTAs (the pipelined step's knob)
     rs_by_ctas = {}
     for ctas in args.reduce_ctas:
@@ -178,7 +186,7 @@ def main():
         "adam_ag_ms": t_up, "ag_busbw_gbs": bus(t_up), "ag_frac_770": bus(t_up) / 770.0,
         "adam_hbm_gbs": 28 * owned / (t_up / 1e3) / 1e9,
         "ce_pull_ms": ce_ms, "ce_pull_busbw_gbs": bus(ce_ms),
-        "reduce_ms_by_persistent_ctas": rs_by_ctas,
+        "reduce_ms_by_persistent_ctas": rs_by_ctas, "adam_ag_ms_by_publish_mode": upd_by_publish,
         "rs_nvlink_bytes_in_per_gpu": S * (n - 1) / n, "ag_nvlink_bytes_out_per_gpu": S * (n - 1) / n,
     }))
 
