@@ -123,7 +123,11 @@ __device__ __forceinline__ void publish1(void* p16, const PeerPtrs& peers, uint6
   if constexpr (PUB == kPubLocal) {
     store1<PDT>(p16, po, x);
   } else {
-    for (int r = 0; r < peers.n; ++r) store1<PDT>(reinterpret_cast<void*>(peers.p[r]), po, x);
+    // constant indices only: a runtime-indexed peers.p[r] would copy the
+    // peer table to local memory and push ptxas into spilling the hot path
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (r < peers.n) store1<PDT>(reinterpret_cast<void*>(peers.p[r]), po, x);
   }
 }
 
@@ -214,7 +218,9 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
         using T = typename Elem<PDT>::T;
         const uint32_t src = (uint32_t)__cvta_generic_to_shared(s_pub);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int r = 0; r < peers.n; ++r) {
+#pragma unroll
+        for (int r = 0; r < kMaxPeers; ++r) {
+          if (r >= peers.n) break;
           T* dst = reinterpret_cast<T*>(peers.p[r]) + po;
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                        ::"l"(dst), "r"(src), "r"(n * (uint32_t)sizeof(T)) : "memory");

@@ -165,8 +165,10 @@ __device__ __forceinline__ void reduce_chunks(const hm_seg_chunk* __restrict__ c
     } else {
       for (uint32_t i = tid; i < c[m].n; i += kThreads) {
         float a = 0.f;
-        for (int r = 0; r < peers.n; ++r)
-          a = __fadd_rn(a, Elem<DT>::widen(reinterpret_cast<const T*>(peers.p[r])[off + i]));
+#pragma unroll
+        for (int r = 0; r < NP; ++r)
+          if (r < peers.n)
+            a = __fadd_rn(a, Elem<DT>::widen(reinterpret_cast<const T*>(peers.p[r])[off + i]));
         const float r = Elem<DT>::widen(Elem<DT>::narrow(a));
         bad |= !is_finite(r);
         sq += __fmul_rn(r, r);
