@@ -2,6 +2,7 @@
 include/hm_page.h declares; the ctypes table covers exactly that set."""
 import ctypes
 import re
+from pathlib import Path
 
 from conftest import ROOT
 from paper_2303_02868_b200 import _native as N
@@ -36,3 +37,23 @@ def test_struct_layouts_match_header():
     assert N.GROUP_LAUNCH.names == ("g_shift", "p_shift", "group", "flag")
     assert N.SEG_CHUNK.names == ("src_off", "dst_off", "n", "slot")
     assert ctypes.sizeof(N.AdamHyperC) == 32
+
+
+def test_kernels_do_not_spill():
+    """Every data-path kernel in the library keeps its working set in
+    registers: no local memory / stack (a spill or a runtime-indexed peer
+    table turns into extra HBM traffic — it once cost the update+AG kernel
+    2 GB per step).  The tiny per-layer flag merge is exempt."""
+    import shutil
+    import subprocess
+    import pytest
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    lib = ROOT / "paper_2303_02868_b200" / "libhm_page.so"
+    if not lib.exists() or not Path(tool).exists():
+        pytest.skip("needs the built library and cuobjdump")
+    out = subprocess.run([tool, "-res-usage", str(lib)], capture_output=True, text=True, check=True).stdout
+    funcs = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+) SHARED:\d+ LOCAL:(\d+)", out)
+    assert len(funcs) > 20
+    bad = [(f, stack, local) for f, _, stack, local in funcs
+           if (int(stack) or int(local)) and "flags_merge" not in f]
+    assert not bad, bad
