@@ -223,7 +223,9 @@ RcFn pick_rc_np(bool persistent) {
 
 template <int DT>
 RcFn pick_rc_dt(bool mc, int n, bool persistent) {
-  if (mc) return reduce_check_kernel<DT, true, 1, 1>;   // one in-switch load per granule
+  // multicast: one in-switch load per granule; NP still bounds the P2P loads of
+  // the unaligned head/tail chunks, which are summed peer by peer
+  if (mc) return reduce_check_kernel<DT, true, kMaxPeers, 1>;
   if (n <= 2) return pick_rc_np<DT, 2>(persistent);
   if (n <= 4) return pick_rc_np<DT, 4>(persistent);
   return pick_rc_np<DT, 8>(persistent);
