@@ -34,7 +34,7 @@ from . import _device as D
 from . import _native as N
 from .errors import ConfigError
 from .layout import PageLayout
-from .lockfree import MasterState, ParamBuffer, SweepResult, _Engine, _Paged
+from .lockfree import MasterState, ParamBuffer, SweepResult, _Paged
 from .pagemem import PAGE_BYTES_DEFAULT
 
 
