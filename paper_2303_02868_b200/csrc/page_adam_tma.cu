@@ -26,19 +26,25 @@ int g_adam_variant = 0;
 
 namespace {
 
-constexpr int kStages = 3;
+constexpr int kMaxStages = 4;
 constexpr int kConsumerWarps = 16;  // the Adam chain is latency-bound per warp: 16 warps hide it
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kTmaThreads = kConsumers + 32;
 
+// One stage = one 4096-element chunk: g | p | m | v, and the 16-bit publish.
+// With a 16-bit gradient each thread writes its published granule over the
+// g granule it has just consumed (same 16 B), so a stage is 56 KB and four
+// stages (224 KB) fit: two chunks loading while one computes and one drains.
 template <int GDT>
 struct StageLayout {
-  static constexpr int kGBytes = kChunk * (GDT == HM_DT_F32 ? 4 : 2);
+  static constexpr bool kF32G = GDT == HM_DT_F32;
+  static constexpr int kGBytes = kChunk * (kF32G ? 4 : 2);
   static constexpr int kOffP = kGBytes;
   static constexpr int kOffM = kOffP + kChunk * 4;
   static constexpr int kOffV = kOffM + kChunk * 4;
-  static constexpr int kOffP16 = kOffV + kChunk * 4;
-  static constexpr int kBytes = kOffP16 + kChunk * 2;
+  static constexpr int kOffP16 = kF32G ? kOffV + kChunk * 4 : 0;
+  static constexpr int kBytes = kOffV + kChunk * 4 + (kF32G ? kChunk * 2 : 0);
+  static constexpr int kStages = kF32G ? 3 : 4;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -119,8 +125,9 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
   constexpr int kGE = GDT == HM_DT_F32 ? 4 : 2;
   constexpr bool kPub = PDT != 0;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  __shared__ int vecflag[kStages];
+  constexpr int kStages = L::kStages;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ int vecflag[kMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -265,7 +272,8 @@ TmaFn pick(int gdt, int pdt) {
 }
 
 int stage_bytes(int gdt) {
-  return kStages * (gdt == HM_DT_F32 ? StageLayout<HM_DT_F32>::kBytes : StageLayout<HM_DT_BF16>::kBytes);
+  return gdt == HM_DT_F32 ? StageLayout<HM_DT_F32>::kStages * StageLayout<HM_DT_F32>::kBytes
+                          : StageLayout<HM_DT_BF16>::kStages * StageLayout<HM_DT_BF16>::kBytes;
 }
 
 }  // namespace
