@@ -1,13 +1,17 @@
 """bench.py's N>1 arm: the data-parallel page step under torchrun (one
-process per GPU, NCCL over NVLink/NVSwitch).
+process per GPU over NVLink/NVSwitch).
 
-Step = reduce-scatter of the bf16 gradient page pool (in place, bucketed) ->
-finite/norm check of the owned reduced pages + per-layer flag all-reduce ->
-prologue -> page-Adam per bucket with the parameter all-gather of bucket b
-overlapped with Adam of bucket b+1.  ``value`` = params of the whole model
-updated per second (strong scaling: the model is fixed, each rank updates
-1/N of its pages); RS/AG bus bandwidths are reported beside it,
-busbw = (S/t)(N-1)/N with S the bytes of the full 16-bit pool.
+Default (``--dp-mode p2p``): sharding.FusedShardedPageStep — reduce-scatter
+of the 16-bit gradient pages fused with the finite/norm check over peer
+memory -> flag merge -> prologue -> page-Adam whose publish epilogue writes
+every peer's pool (the all-gather); at N=2 pipelined over layer groups
+(``--dp-groups -1`` = the measured policy).  ``--dp-mode nccl``:
+sharding.ShardedPageStep (NCCL RS, check, flag all-reduce, page-Adam per
+bucket with the AG of bucket b overlapped with Adam of bucket b+1).
+``value`` = params of the whole model updated per second (strong scaling:
+the model is fixed, each rank updates 1/N of its pages); RS/AG bus
+bandwidths are reported beside it, busbw = (S/t)(N-1)/N with S = 2 B x
+params (the algorithmic payload).
 
 Synthetic gradients: each rank holds non-zero gradients only in the pages it
 owns, so the in-place reduce-scatter returns every owner its own values and
@@ -206,6 +210,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "algorithmic_bytes": S, "pool_bytes_padded": pool_bytes,
                    "link_bound_ms": 2 * S * (world - 1) / world / 770e9 * 1e3},
         "components_ms": parts,
+        "reference_model": _reference_model(layout, page, world),
         "clocks": clk.summary(),
         "gpu_launches": args.steps * ((2 + layout.num_buckets) if not fused else
                                      4 * (args.dp_groups if pipelined else 1)),
@@ -247,3 +252,20 @@ def run_e2e(args, buf, ms, do_step, flat, layout):
             "steps": args.e2e_steps, "h2d_gbs_per_rank": h2d / dt / 1e9,
             "api": "ParamBuffer.accumulate_flat(pinned host gradient) + sharded page step + "
                    "applied flags to host, every rank"}
+
+
+def _reference_model(layout, page, world):
+    """The reference simulator's view of the same exchange (per-page gather
+    tasks on one interconnect resource, hiermem/simengine.py:255-257) with the
+    measured B200 link of presets/b200-server.json — printed next to the
+    measured step so the model can be checked."""
+    from pathlib import Path
+    from .sharding import modeled_gather_s
+    preset = Path(__file__).resolve().parent.parent / "presets" / "b200-server.json"
+    try:
+        link = json.loads(preset.read_text())["links"]["gpu_interconnect"]
+    except (OSError, KeyError, ValueError):
+        return None
+    ag = modeled_gather_s(page, layout.used_pages, world, link["bandwidth_bytes_per_s"], link["latency_s"])
+    return {"preset": "presets/b200-server.json", "ag_ms": ag * 1e3, "rs_ms": ag * 1e3,
+            "comm_ms": 2 * ag * 1e3, "formula": "pages x (lat + page (N-1)/N / bw) per collective"}

@@ -54,6 +54,19 @@ class ShardingModel:
         return self.owner(page_id) == self.rank
 
 
+def modeled_gather_s(page_bytes: int, pages: int, world_size: int, bandwidth_bytes_per_s: float,
+                     latency_s: float) -> float:
+    """The reference's cost of gathering ``pages`` pages: one
+    ``latency + page·(N−1)/N / bw`` task per page, serialised on the single
+    ``gpu_interconnect`` resource (hiermem/simengine.py:255-257; a
+    reduce-scatter moves the same bytes the other way).  bench.py prints it
+    beside the measured fused step so the model can be checked against B200."""
+    if world_size < 1 or pages < 0 or bandwidth_bytes_per_s <= 0:
+        raise ConfigError("modeled_gather_s: bad arguments")
+    frac = (world_size - 1) / world_size
+    return pages * (latency_s + page_bytes * frac / bandwidth_bytes_per_s)
+
+
 class PageCollectives:
     """In-place bucketed reduce-scatter / all-gather of a 16-bit page pool."""
 

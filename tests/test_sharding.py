@@ -110,3 +110,14 @@ def test_bucketed_rs_ag_world2_gloo(K):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+def test_modeled_gather_matches_reference_formula():
+    """hiermem/simengine.py:255-257: one lat + page*(N-1)/N/bw task per page."""
+    from paper_2303_02868_b200.sharding import modeled_gather_s
+    page, pages, lat, bw = 4 << 20, 676, 10e-6, 770e9
+    for n in (1, 2, 4, 8):
+        want = sum(lat + page * ((n - 1) / n) / bw for _ in range(pages))
+        assert abs(modeled_gather_s(page, pages, n, bw, lat) - want) < 1e-12
+    with pytest.raises(ConfigError):
+        modeled_gather_s(page, pages, 0, bw, lat)
