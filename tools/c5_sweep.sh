@@ -8,7 +8,7 @@ for P in ${PAGES:-1 2 4 8 16 32 64}; do
       > gpurun_out/c5_n1_p$P.log 2>&1
   else
     timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29503 \
-      bench.py --gpus $N --config c5 --page-mib $P --steps 10 --warmup 3 --dp-mode ${MODE:-p2p} --bucket-pages 4 \
+      bench.py --gpus $N --config c5 --page-mib $P --steps 10 --warmup 3 --dp-mode ${MODE:-p2p} --bucket-pages 4 --e2e-steps 0 \
       > gpurun_out/c5_n${N}_p$P.log 2>&1
   fi
 done
