@@ -63,6 +63,10 @@ def main():
                 g = rr.normal(0, 1e-2, n).astype(np.float32)
                 if it == 1 and l == 6 and r == world - 1:
                     g[3] = np.inf   # one rank's non-finite gradient rejects the layer everywhere
+                if it == 2 and l == 3 and r in (0, 1):
+                    # finite on every rank, but the reduced sum overflows the
+                    # 16-bit type: the rounded sum is inf and the layer is rejected
+                    g[7] = 60000.0 if dtype == "fp16" else 3.0e38
                 gs.append(O.to16(g, dtype))
             per_rank.append(gs)
         mine = per_rank[rank]
