@@ -235,6 +235,11 @@ int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_grou
  * writes to complete before it retires.  Same bytes, same results.
  * Process-wide. */
 int hm_set_ag_publish(int mode);
+/* Grid of hm_adam_main_ag (per-thread peer stores or multicast): 0 (default)
+ * = one CTA per chunk; ctas > 0 = a persistent grid striding over the chunks,
+ * so the update of one layer group takes a fixed share of the SMs beside the
+ * persistent reduce of the next.  Process-wide. */
+int hm_set_dp_update_ctas(int ctas);
 
 /* Elementwise segment chunk used by accumulate / cast / reduce. */
 typedef struct hm_seg_chunk {

@@ -93,6 +93,7 @@ constexpr int kPubLocal = 0, kPubPeers = 1, kPubMulticast = 2, kPubPeersBulk = 3
 template <int PUB>
 constexpr bool is_bulk() { return PUB == kPubPeersBulk || PUB == kPubPeersBulkWait; }
 int g_ag_publish = 0;   // hm_set_ag_publish: 0 per-thread stores; 1 bulk; 2 bulk + full wait
+int g_update_ctas = 0;  // hm_set_dp_update_ctas: 0 one CTA per chunk; >0 persistent grid
 
 template <int PDT, int PUB>
 __device__ __forceinline__ void publish8(void* p16, const PeerPtrs& peers, char* mc, uint64_t po,
@@ -133,13 +134,14 @@ __device__ __forceinline__ void publish1(void* p16, const PeerPtrs& peers, uint6
 
 // NT threads per 4096-element chunk: 256 (2 granules/thread, all 7 loads of
 // both issued up front) or 512 (1 granule/thread, more warps to hide latency).
-template <int GDT, int PDT, int PUB = kPubLocal, int NT = kThreads>
-__global__ void __launch_bounds__(NT)
-adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ groups,
-          const hm_group_rt* __restrict__ rt, const void* __restrict__ g,
-          float* __restrict__ p32, float* __restrict__ m32, float* __restrict__ v32,
-          void* __restrict__ p16, hm_adam_hyper hyper, PeerPtrs peers, char* mc) {
-  const hm_adam_chunk c = chunks[blockIdx.x];
+template <int GDT, int PDT, int PUB, int NT>
+__device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
+                                           const hm_group_launch* __restrict__ groups,
+                                           const hm_group_rt* __restrict__ rt,
+                                           const void* __restrict__ g, float* __restrict__ p32,
+                                           float* __restrict__ m32, float* __restrict__ v32,
+                                           void* __restrict__ p16, const hm_adam_hyper& hyper,
+                                           const PeerPtrs& peers, char* mc) {
   const hm_group_launch gl = groups[c.slot];
   const hm_group_rt r = rt[c.slot];
   const uint64_t go = c.g_off + gl.g_shift;
@@ -245,6 +247,32 @@ adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __res
   }
 }
 
+template <int GDT, int PDT, int PUB = kPubLocal, int NT = kThreads>
+__global__ void __launch_bounds__(NT)
+adam_main(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ groups,
+          const hm_group_rt* __restrict__ rt, const void* __restrict__ g,
+          float* __restrict__ p32, float* __restrict__ m32, float* __restrict__ v32,
+          void* __restrict__ p16, hm_adam_hyper hyper, PeerPtrs peers, char* mc) {
+  adam_chunk<GDT, PDT, PUB, NT>(chunks[blockIdx.x], groups, rt, g, p32, m32, v32, p16, hyper,
+                                peers, mc);
+}
+
+// Persistent form for the layer-group pipelined DP step: a grid of
+// hm_set_dp_update_ctas CTAs strides over the chunks, so the update of group
+// k occupies a fixed share of the SMs next to the persistent reduce of
+// group k+1 instead of competing for every free slot.
+template <int GDT, int PDT, int PUB>
+__global__ void __launch_bounds__(kThreads)
+adam_main_loop(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
+               const hm_group_launch* __restrict__ groups, const hm_group_rt* __restrict__ rt,
+               const void* __restrict__ g, float* __restrict__ p32, float* __restrict__ m32,
+               float* __restrict__ v32, hm_adam_hyper hyper, PeerPtrs peers, char* mc) {
+  static_assert(!is_bulk<PUB>(), "the staged bulk epilogue reuses shared memory per chunk");
+  for (int i = blockIdx.x; i < n_chunks; i += gridDim.x)
+    adam_chunk<GDT, PDT, PUB, kThreads>(chunks[i], groups, rt, g, p32, m32, v32, nullptr, hyper,
+                                        peers, mc);
+}
+
 using AdamFn = void (*)(const hm_adam_chunk*, const hm_group_launch*, const hm_group_rt*,
                         const void*, float*, float*, float*, void*, hm_adam_hyper, PeerPtrs, char*);
 
@@ -257,6 +285,17 @@ AdamFn pick_adam_ag_dt(int pub) {
     case kPubPeersBulkWait: return adam_main<DT, DT, kPubPeersBulkWait>;
   }
   return nullptr;
+}
+
+using AdamLoopFn = void (*)(const hm_adam_chunk*, int, const hm_group_launch*, const hm_group_rt*,
+                           const void*, float*, float*, float*, hm_adam_hyper, PeerPtrs, char*);
+
+AdamLoopFn pick_adam_ag_loop(int dt, int pub) {
+  if (dt == HM_DT_BF16)
+    return pub == kPubPeers ? adam_main_loop<HM_DT_BF16, HM_DT_BF16, kPubPeers>
+                            : adam_main_loop<HM_DT_BF16, HM_DT_BF16, kPubMulticast>;
+  return pub == kPubPeers ? adam_main_loop<HM_DT_F16, HM_DT_F16, kPubPeers>
+                          : adam_main_loop<HM_DT_F16, HM_DT_F16, kPubMulticast>;
 }
 
 AdamFn pick_adam_ag(int gdt, int pdt, int pub) {
@@ -351,6 +390,12 @@ extern "C" int hm_set_adam_threads(int threads) {
   return HM_OK;
 }
 
+extern "C" int hm_set_dp_update_ctas(int ctas) {
+  if (ctas < 0) return hm_set_error(HM_ERR_INVALID, "hm_set_dp_update_ctas: negative grid %d", ctas);
+  hm::g_update_ctas = ctas;
+  return HM_OK;
+}
+
 extern "C" int hm_set_ag_publish(int mode) {
   if (mode < 0 || mode > 2)
     return hm_set_error(HM_ERR_INVALID, "hm_set_ag_publish: 0, 1 or 2, got %d", mode);
@@ -374,6 +419,15 @@ extern "C" int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks,
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: bad chunk count");
   if (n_chunks == 0) return HM_OK;
+  if (hm::g_update_ctas > 0 && (pub == hm::kPubPeers || pub == hm::kPubMulticast)) {
+    hm::AdamLoopFn lf = hm::pick_adam_ag_loop(g_dtype, pub);
+    const int64_t grid = hm::g_update_ctas < n_chunks ? hm::g_update_ctas : n_chunks;
+    lf<<<(unsigned)grid, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        chunks, (int)n_chunks, groups, rt, g, p32, m32, v32, *hyper, peers,
+        static_cast<char*>(mc_p16));
+    HM_CUDA_CHECK_LAUNCH();
+    return HM_OK;
+  }
   fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, groups, rt, g, p32, m32, v32, nullptr, *hyper, peers, static_cast<char*>(mc_p16));
   HM_CUDA_CHECK_LAUNCH();

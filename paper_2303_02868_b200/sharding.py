@@ -6,20 +6,23 @@ Ownership is the reference's ``ShardingModel``: ``owner(page) = page % N``
 685).  The reference only *models* the collectives — an all_gather task per
 page costed as ``lat + page*(N-1)/N / bw`` (hiermem/simengine.py:255-257) and
 no gradient reduce-scatter at all (SPEC.md:348 lists it as future work).
-Here they are real NCCL collectives over NVLink/NVSwitch on the page pools:
+Here they move real bytes over NVLink/NVSwitch, two ways:
 
-* the 16-bit pools are laid out bucket-major, rank-major inside a bucket
-  (layout.py), so bucket b is ONE contiguous buffer and rank r's owned pages
-  are its r-th block: ``reduce_scatter_tensor`` / ``all_gather_into_tensor``
-  run in place with no packing copies;
-* the DP step is  RS(all buckets) -> finite/norm check of the owned reduced
-  pages -> all-reduce of the per-layer flags (tiny) -> ONE prologue ->
-  for each bucket: page-Adam(b) on the compute stream || AG(b) on the comm
-  stream once Adam(b) is done — the transfer of bucket b overlaps the
-  update of bucket b+1.
+* ``FusedShardedPageStep`` (the default): the pools are symmetric memory
+  mapped into every rank; the reduce-scatter is a kernel that pulls each
+  owned page from every peer and fuses the finite flag / norm
+  (hm_dp_reduce_check), and the all-gather is the page-Adam's publish
+  epilogue storing into every peer (hm_adam_main_ag) — no NCCL on the data
+  path; optionally pipelined over layer groups (``step_pipelined``);
+* ``ShardedPageStep`` (NCCL baseline): the 16-bit pools are laid out
+  bucket-major, rank-major inside a bucket (layout.py), so bucket b is ONE
+  contiguous buffer and rank r's owned pages are its r-th block:
+  ``reduce_scatter_tensor`` / ``all_gather_into_tensor`` run in place; the
+  step is RS(all buckets) -> finite/norm check -> all-reduce of the
+  per-layer flags -> ONE prologue -> page-Adam(b) || AG(b) per bucket.
 
 ``PageCollectives`` is device-agnostic (it runs on CPU tensors under gloo in
-the tests); ``ShardedPageStep`` drives the CUDA kernels.
+the tests); the two step classes drive the CUDA kernels.
 """
 from __future__ import annotations
 
@@ -303,7 +306,8 @@ class FusedShardedPageStep:
                              torch.cuda.Stream(self.device))
         return cache[groups]
 
-    def step_pipelined(self, hyper, groups: int = 4, *, reduce_ctas: int = 0, stream=None,
+    def step_pipelined(self, hyper, groups: int = 4, *, reduce_ctas: int = 0, update_ctas: int = 0,
+                       stream=None,
                        timings: dict | None = None):
         """``step`` with the layers cut into contiguous groups and two streams:
         the reduce-scatter + check of group k+1 runs while group k is updated
@@ -313,7 +317,8 @@ class FusedShardedPageStep:
         streams, so ``reduce_ctas > 0`` launches the reduce as a persistent
         grid of that many CTAs on a high-priority stream: the link-bound
         reduce then runs from a few SMs beside the HBM-bound update of the
-        previous group.  With NVLS the RS leg is outbound-heavy (S out, S/N
+        previous group; ``update_ctas > 0`` likewise gives the update a
+        persistent grid of its own.  With NVLS the RS leg is outbound-heavy (S out, S/N
         in per GPU) and the AG leg inbound-heavy (S/N out, S in), so
         overlapping them moves (1 + 1/N)·S per link direction instead of
         2·(N−1)/N·S."""
@@ -355,6 +360,7 @@ class FusedShardedPageStep:
         hc = D.hyper_c(hyper)
         rts = self.__dict__.setdefault("_rts", {})
         D.check(lib.hm_set_dp_reduce_ctas(int(reduce_ctas)))   # persistent reduce grid (0 = per chunk)
+        D.check(lib.hm_set_dp_update_ctas(int(update_ctas)))   # persistent update grid (0 = per chunk)
         for k, (grp, check, adam) in enumerate(plan):
             first, n = grp[0], len(grp)
             with torch.cuda.stream(rs):
@@ -384,6 +390,7 @@ class FusedShardedPageStep:
                                             self.n, self.mc_p if self.mc_p else None, buf._dt, hc,
                                             D.sptr(up)))
         D.check(lib.hm_set_dp_reduce_ctas(0))
+        D.check(lib.hm_set_dp_update_ctas(0))
         mark("rs", rs)
         st.wait_stream(rs)
         st.wait_stream(up)

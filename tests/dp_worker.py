@@ -78,7 +78,8 @@ def main():
         gsel = buf._gsel[0]
         groups = int(os.environ.get("DP_GROUPS", "1"))
         if groups > 1 and mode != "nccl":
-            step.step_pipelined(hyper, groups, reduce_ctas=int(os.environ.get("DP_REDUCE_CTAS", "0")))
+            step.step_pipelined(hyper, groups, reduce_ctas=int(os.environ.get("DP_REDUCE_CTAS", "0")),
+                                update_ctas=int(os.environ.get("DP_UPDATE_CTAS", "0")))
         else:
             step.step(hyper)
         # every owner's reduced (post reduce-scatter) pages, gathered so each

@@ -19,17 +19,21 @@ ROOT = Path(__file__).resolve().parent.parent
     (2, "bf16", "p2p", 1, 0), (2, "fp16", "p2p", 1, 0), (3, "bf16", "nvls", 1, 0),
     (2, "bf16", "p2p", 3, 0), (2, "bf16", "nvls", 4, 0),
     (2, "bf16", "p2p", 3, 5),    # persistent reduce grid: 5 CTAs striding over the chunks
-    (2, "bf16", "p2p", 1, "bulk1"), (2, "fp16", "p2p", 3, "bulk2")])   # bulk-copy AG epilogue
+    (2, "bf16", "p2p", 1, "bulk1"), (2, "fp16", "p2p", 3, "bulk2"),    # bulk-copy AG epilogue
+    (2, "bf16", "p2p", 3, "upd7")])   # persistent update grid (7 CTAs) + persistent reduce (5)
 def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
-    agp = 0
-    if isinstance(ctas, str):
+    agp, upd = 0, 0
+    if isinstance(ctas, str) and ctas.startswith("bulk"):
         agp, ctas = int(ctas[-1]), 0
+    elif isinstance(ctas, str):
+        upd, ctas = int(ctas[3:]), 5
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = 4 if n >= 4 else 2
     env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype, DP_MODE=mode, DP_GROUPS=str(groups),
-               DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp))
+               DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp),
+               DP_UPDATE_CTAS=str(upd))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29611", str(ROOT / "tests" / "dp_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
