@@ -2,7 +2,10 @@
 and refresh profiles/ncu_traffic.json (DRAM bytes of one adam_main launch,
 read by bench.py as roofline.traffic).
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r1_ncu_full_c2.txt "<command>"
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r1_ncu_full_c2.txt "<command>" [--no-traffic]
+
+--no-traffic: summarise only (reports of the DP kernels, whose adam_main is
+the owned-page update+all-gather, must not overwrite the C2 traffic figure).
 """
 import csv
 import io
@@ -15,12 +18,15 @@ KEYS = ["launch__grid_size", "launch__block_size", "launch__registers_per_thread
         "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second", "dram__cycles_elapsed.avg.per_second"]
+        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second", "dram__cycles_elapsed.avg.per_second",
+        "nvlrx__bytes.sum", "nvltx__bytes.sum", "nvlrx__bytes_data_user.sum", "nvltx__bytes_data_user.sum"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def main():
-    rep, out, cmd = sys.argv[1], Path(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else ""
+    args = [a for a in sys.argv[1:] if a != "--no-traffic"]
+    refresh = "--no-traffic" not in sys.argv
+    rep, out, cmd = args[0], Path(args[1]), args[2] if len(args) > 2 else ""
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -42,7 +48,7 @@ def main():
         if "adam_main" in name:
             traffic.setdefault("adam_main", total)
     out.write_text("\n".join(lines) + "\n")
-    if "adam_main" in traffic:
+    if refresh and "adam_main" in traffic:
         tj = out.parent / "ncu_traffic.json"
         d = json.loads(tj.read_text()) if tj.exists() else {}
         d["c2:bf16"] = traffic["adam_main"]
