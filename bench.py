@@ -267,13 +267,20 @@ def run_ours_single(args):
     # K3 producer throughput (accumulate into pages, fused finite flag + norm).
     torch.cuda.synchronize()
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for l in range(L):
-        buf._pending[l] = 0
+    acc_reps = 5   # back to back, so the host-side launch work overlaps the previous launch
+
+    def first_message():
+        for l in range(L):
+            buf._pending[l] = 0
+        buf.accumulate_flat(grads, 0)
+    first_message()
+    torch.cuda.synchronize()
     a0.record(stream)
-    buf.accumulate_flat(grads, 0)
+    for _ in range(acc_reps):
+        first_message()
     a1.record(stream)
     torch.cuda.synchronize()
-    acc_ms = a0.elapsed_time(a1)
+    acc_ms = a0.elapsed_time(a1) / acc_reps
     LF.sweep(buf, ms, hyper)
 
     e2e = run_e2e(args, buf, ms, hyper, grads, device) if args.e2e_steps > 0 else None
