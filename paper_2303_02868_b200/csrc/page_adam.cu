@@ -16,6 +16,8 @@
 // The whole-layer reject of lockfree.py:133-134 (+ step rollback :163-164) is
 // decided once per layer by the prologue from the flag that the gradient's
 // producer (hm_accumulate / hm_reduce_stats) fused into its own pass.
+#include <atomic>
+
 #include "hm_adam.cuh"
 #include "hm_device.cuh"
 #include "hm_dp.cuh"
@@ -92,8 +94,10 @@ constexpr int kPubLocal = 0, kPubPeers = 1, kPubMulticast = 2, kPubPeersBulk = 3
               kPubPeersBulkWait = 4;   // bulk + wait for the remote writes before the CTA retires
 template <int PUB>
 constexpr bool is_bulk() { return PUB == kPubPeersBulk || PUB == kPubPeersBulkWait; }
-int g_ag_publish = 0;   // hm_set_ag_publish: 0 per-thread stores; 1 bulk; 2 bulk + full wait
-int g_update_ctas = 0;  // hm_set_dp_update_ctas: 0 one CTA per chunk; >0 persistent grid
+// Process-wide tuning knobs (atomic: set from any host thread; each launch
+// reads a knob once, so a concurrent change never mixes two settings).
+std::atomic<int> g_ag_publish{0};   // hm_set_ag_publish: 0 per-thread stores; 1 bulk; 2 bulk + full wait
+std::atomic<int> g_update_ctas{0};  // hm_set_dp_update_ctas: 0 one CTA per chunk; >0 persistent grid
 
 template <int PDT, int PUB>
 __device__ __forceinline__ void publish8(void* p16, const PeerPtrs& peers, char* mc, uint64_t po,
@@ -305,7 +309,7 @@ AdamFn pick_adam_ag(int gdt, int pdt, int pub) {
   return nullptr;
 }
 
-int g_adam_threads = kThreads;  // tuning knob: hm_set_adam_threads
+std::atomic<int> g_adam_threads{kThreads};  // tuning knob: hm_set_adam_threads
 
 template <int GDT, int NT>
 AdamFn pick_p(int pdt) {
@@ -327,8 +331,8 @@ AdamFn pick_adam_nt(int gdt, int pdt) {
   return nullptr;
 }
 
-AdamFn pick_adam(int gdt, int pdt) {
-  return g_adam_threads == 512 ? pick_adam_nt<512>(gdt, pdt) : pick_adam_nt<kThreads>(gdt, pdt);
+AdamFn pick_adam(int gdt, int pdt, int threads) {
+  return threads == 512 ? pick_adam_nt<512>(gdt, pdt) : pick_adam_nt<kThreads>(gdt, pdt);
 }
 
 }  // namespace
@@ -370,14 +374,15 @@ extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_adam_main: bad chunk count %lld", (long long)n_chunks);
   const int pdt = p16 ? p16_dtype : 0;
-  hm::AdamFn fn = hm::pick_adam(g_dtype, pdt);
+  const int threads = hm::g_adam_threads.load(std::memory_order_relaxed);
+  hm::AdamFn fn = hm::pick_adam(g_dtype, pdt, threads);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (n_chunks == 0) return HM_OK;
-  if (hm::g_adam_variant == 1)
+  if (hm::g_adam_variant.load(std::memory_order_relaxed) == 1)
     return hm::launch_adam_tma(chunks, n_chunks, groups, rt, g, g_dtype, p32, m32, v32, p16, p16_dtype,
                                *hyper, static_cast<cudaStream_t>(stream));
   hm::PeerPtrs none{};
-  fn<<<(unsigned)n_chunks, hm::g_adam_threads, 0, static_cast<cudaStream_t>(stream)>>>(
+  fn<<<(unsigned)n_chunks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, groups, rt, g, p32, m32, v32, p16, *hyper, none, nullptr);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
@@ -411,17 +416,19 @@ extern "C" int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks,
   if (!hyper || !rt) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: missing hyper/rt");
   hm::PeerPtrs peers;
   if (int rc = hm::make_peers(peer_p16, n_peers, &peers)) return rc;
+  const int agp = hm::g_ag_publish.load(std::memory_order_relaxed);
   const int pub = mc_p16 ? hm::kPubMulticast
-                 : hm::g_ag_publish == 1 ? hm::kPubPeersBulk
-                 : hm::g_ag_publish == 2 ? hm::kPubPeersBulkWait : hm::kPubPeers;
+                 : agp == 1 ? hm::kPubPeersBulk
+                 : agp == 2 ? hm::kPubPeersBulkWait : hm::kPubPeers;
   hm::AdamFn fn = hm::pick_adam_ag(g_dtype, p16_dtype, pub);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: unsupported dtypes g=%d p16=%d", g_dtype, p16_dtype);
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: bad chunk count");
   if (n_chunks == 0) return HM_OK;
-  if (hm::g_update_ctas > 0 && (pub == hm::kPubPeers || pub == hm::kPubMulticast)) {
+  const int uctas = hm::g_update_ctas.load(std::memory_order_relaxed);
+  if (uctas > 0 && (pub == hm::kPubPeers || pub == hm::kPubMulticast)) {
     hm::AdamLoopFn lf = hm::pick_adam_ag_loop(g_dtype, pub);
-    const int64_t grid = hm::g_update_ctas < n_chunks ? hm::g_update_ctas : n_chunks;
+    const int64_t grid = uctas < n_chunks ? uctas : n_chunks;
     lf<<<(unsigned)grid, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         chunks, (int)n_chunks, groups, rt, g, p32, m32, v32, *hyper, peers,
         static_cast<char*>(mc_p16));
@@ -443,7 +450,7 @@ extern "C" int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                             uint32_t* nonfinite, double* sumsq, int consume_flags,
                             void* stream) {
   const int pdt = p16 ? p16_dtype : 0;
-  if (!hm::pick_adam(g_dtype, pdt))
+  if (!hm::pick_adam(g_dtype, pdt, hm::kThreads))   // dtype check only
     return hm_set_error(HM_ERR_INVALID, "hm_adam_step: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (int rc = hm_adam_prologue(groups, n_groups, rt_scratch, hyper, bc_table, bc_len,
                                 explicit_step, steps, applied, nonfinite, sumsq, consume_flags,

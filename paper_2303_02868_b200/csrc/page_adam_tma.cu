@@ -22,7 +22,7 @@
 
 namespace hm {
 
-int g_adam_variant = 0;
+std::atomic<int> g_adam_variant{0};
 
 namespace {
 

@@ -17,6 +17,8 @@
 // The reference only models these transfers (hiermem/simengine.py:255-257,
 // all_gather = lat + page*(N-1)/N / bw) and has no reduce-scatter
 // (SPEC.md:348); ownership is hiermem/scheduler.py:72-76 (page % N).
+#include <atomic>
+
 #include "hm_device.cuh"
 #include "hm_dp.cuh"
 #include "hm_error.h"
@@ -209,7 +211,7 @@ __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, in
 
 using RcFn = void (*)(const hm_seg_chunk*, int, PeerPtrs, const char*, void*, uint32_t*, double*);
 
-int g_reduce_ctas = 0;   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
+std::atomic<int> g_reduce_ctas{0};   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
 
 // Chunks per pass of the persistent grid: as deep as the registers allow.
 template <int NP>
@@ -261,12 +263,13 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: bad chunk count");
   if (n_chunks == 0) return HM_OK;
-  const bool persistent = hm::g_reduce_ctas > 0;
+  const int rctas = hm::g_reduce_ctas.load(std::memory_order_relaxed);
+  const bool persistent = rctas > 0;
   int depth = 1;
   hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, n_peers, persistent, &depth);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
   const int64_t passes = (n_chunks + depth - 1) / depth;
-  const int64_t grid = persistent && hm::g_reduce_ctas < passes ? hm::g_reduce_ctas : passes;
+  const int64_t grid = persistent && rctas < passes ? rctas : passes;
   fn<<<(unsigned)grid, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, (int)n_chunks, peers, static_cast<const char*>(mc_pool), local_pool, nonfinite, sumsq);
   HM_CUDA_CHECK_LAUNCH();
