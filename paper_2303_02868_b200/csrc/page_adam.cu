@@ -359,6 +359,7 @@ extern "C" int hm_adam_prologue(const hm_group_launch* groups, int32_t n_groups,
                                 double* sumsq, int consume_flags, void* stream) {
   if (int rc = prologue_args_ok(hyper, bc_table, bc_len, rt_scratch, n_groups, explicit_step, steps))
     return rc;
+  HM_REQUIRE_PTRS("hm_adam_prologue", groups);
   hm::adam_prologue<<<1, hm::kPrologueThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       groups, n_groups, rt_scratch, *hyper, bc_table, bc_len, explicit_step, steps, applied,
       nonfinite, sumsq, consume_flags);
@@ -378,6 +379,7 @@ extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
   hm::AdamFn fn = hm::pick_adam(g_dtype, pdt, threads);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (n_chunks == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_adam_main", chunks, groups, g, p32, m32, v32);
   if (hm::g_adam_variant.load(std::memory_order_relaxed) == 1)
     return hm::launch_adam_tma(chunks, n_chunks, groups, rt, g, g_dtype, p32, m32, v32, p16, p16_dtype,
                                *hyper, static_cast<cudaStream_t>(stream));
@@ -425,6 +427,7 @@ extern "C" int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks,
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: bad chunk count");
   if (n_chunks == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_adam_main_ag", chunks, groups, g, p32, m32, v32);
   const int uctas = hm::g_update_ctas.load(std::memory_order_relaxed);
   if (uctas > 0 && (pub == hm::kPubPeers || pub == hm::kPubMulticast)) {
     hm::AdamLoopFn lf = hm::pick_adam_ag_loop(g_dtype, pub);

@@ -263,6 +263,7 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: bad chunk count");
   if (n_chunks == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_dp_reduce_check", local_pool, chunks);
   const int rctas = hm::g_reduce_ctas.load(std::memory_order_relaxed);
   const bool persistent = rctas > 0;
   int depth = 1;
@@ -293,6 +294,7 @@ int hm_dp_flags_merge(const uint64_t* peer_flags, const uint64_t* peer_sumsq, in
     sumsq_out = nullptr;
   }
   if (n_layers <= 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_dp_flags_merge", flags_out);
   const int blocks = (n_layers + 255) / 256;
   hm::flags_merge_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(f, s, n_layers,
                                                                                 flags_out, sumsq_out);

@@ -328,6 +328,7 @@ int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
   hm::AccFn fn = hm::pick_acc(src_dtype, dst_dtype);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_accumulate: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
   if (n_chunks == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_accumulate", src, dst, chunks);
   fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, src, dst, mode ? 1 : 0, slot_modes, nonfinite, sumsq);
   HM_CUDA_CHECK_LAUNCH();
@@ -340,6 +341,7 @@ int hm_cast(const void* src, int src_dtype, void* dst, int dst_dtype, const hm_s
   hm::CastFn fn = hm::pick_cast(src_dtype, dst_dtype);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_cast: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
   if (n_chunks == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_cast", src, dst, chunks);
   fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, dst);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
@@ -351,6 +353,7 @@ int hm_reduce_stats(const void* src, int src_dtype, const hm_seg_chunk* chunks, 
   hm::RedFn fn = hm::pick_red(src_dtype);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_reduce_stats: unsupported dtype %d", src_dtype);
   if (n_chunks == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_reduce_stats", src, chunks);
   fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, nonfinite,
                                                                                  sums, sumsq);
   HM_CUDA_CHECK_LAUNCH();
@@ -361,6 +364,7 @@ int hm_copy_runs(const void* src, void* dst, const hm_copy_desc* descs, int64_t 
                  void* stream) {
   if (int rc = hm::check_grid(n_descs, "hm_copy_runs")) return rc;
   if (n_descs == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_copy_runs", src, dst, descs);
   hm::copy_runs_kernel<<<(unsigned)n_descs, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const char*>(src), static_cast<char*>(dst), descs);
   HM_CUDA_CHECK_LAUNCH();

@@ -57,3 +57,22 @@ def test_kernels_do_not_spill():
     bad = [(f, stack, local) for f, _, stack, local in funcs
            if (int(stack) or int(local)) and "flags_merge" not in f]
     assert not bad, bad
+
+
+def test_null_pointers_rejected_before_launch():
+    """Argument validation happens on the host, before any CUDA call, so it
+    runs here without a GPU: a null buffer with work to do is HM_ERR_INVALID
+    (never a kernel fault), and an empty launch is a no-op."""
+    lib = N.lib()
+    INVALID = 7
+    assert lib.hm_accumulate(None, 2, None, 2, None, 1, 0, None, None, None, None) == INVALID
+    assert b"null pointer" in lib.hm_last_error()
+    assert lib.hm_cast(None, 3, None, 2, None, 5, None) == INVALID
+    assert lib.hm_reduce_stats(None, 2, None, 3, None, None, None, None) == INVALID
+    assert lib.hm_copy_runs(None, None, None, 2, None) == INVALID
+    assert lib.hm_accumulate(None, 2, None, 2, None, 0, 0, None, None, None, None) == 0
+    assert lib.hm_cast(None, 3, None, 2, None, 0, None) == 0
+    assert lib.hm_accumulate(None, 9, None, 2, None, 1, 0, None, None, None, None) == INVALID
+    assert lib.hm_set_dp_reduce_ctas(-1) == INVALID and lib.hm_set_dp_reduce_ctas(0) == 0
+    assert lib.hm_set_ag_publish(3) == INVALID and lib.hm_set_ag_publish(0) == 0
+    assert lib.hm_set_adam_threads(300) == INVALID
