@@ -166,7 +166,11 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     else:
         rs_ms = timed(lambda: dp.coll.reduce_scatter(gpool))
         ag_ms = timed(lambda: dp.coll.all_gather(ppool))
-    e2e = run_e2e(args, buf, ms, do_step, flat, layout) if args.e2e_steps > 0 else None
+    pipe = None
+    if fused:
+        pipe = lambda ready: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
+                                               ready=ready)
+    e2e = run_e2e(args, buf, ms, do_step, flat, layout, pipe) if args.e2e_steps > 0 else None
     # busbw counts the ALGORITHMIC bytes S = 2 B x params; the
     # padded pool (whole buckets) is larger, but the fused kernels never move
     # the padding and NCCL's extra bytes are overhead, not useful traffic
@@ -225,34 +229,55 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     dist.destroy_process_group()
 
 
-def run_e2e(args, buf, ms, do_step, flat, layout):
+def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
     """The DP step through the public API with host buffers, per rank: H2D of
-    this rank's whole 16-bit gradient from pinned memory + K3 accumulate
-    (``ParamBuffer.accumulate_flat``), the sharded page step, and a D2H read
-    of the per-layer applied flags.  Time = max over ranks of the wall time
-    between synchronised barriers."""
+    this rank's whole 16-bit gradient from pinned memory + K3 accumulate, the
+    sharded page step, and a D2H read of the per-layer applied flags.  Time =
+    max over ranks of the wall time between synchronised barriers.
+
+    serial:    ``ParamBuffer.accumulate_flat(host)`` then the step;
+    pipelined: ``lockfree.ingest`` (per layer group: H2D -> K3, one event per
+               group) feeding ``step_pipelined(ready=...)``, so the reduce,
+               update and all-gather of group k run while group k+1 is still
+               crossing PCIe (fused mode only).  The headline is the faster."""
+    from . import lockfree as LF
     host = flat.cpu().pin_memory()
     h2d = host.numel() * host.element_size()
 
-    def step(it):
+    def serial(it):
         buf.accumulate_flat(host, it)      # H2D (non_blocking from pinned) + K3
         do_step()
         return ms._applied.cpu()           # D2H of the step's result
 
-    for it in range(2):
-        step(it)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t0 = time.perf_counter()
-    for it in range(args.e2e_steps):
-        step(it)
-    torch.cuda.synchronize()
-    dt = _max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+    def pipelined(it):
+        ready = LF.ingest(buf, host, it, groups=args.e2e_groups)
+        pipe(ready)
+        return ms._applied.cpu()
+
+    def timed(step):
+        for it in range(2):
+            step(it)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for it in range(args.e2e_steps):
+            step(it)
+        torch.cuda.synchronize()
+        return _max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+
+    dt_serial = timed(serial)
+    dt_pipe = timed(pipelined) if pipe is not None else None
+    dt = min(dt_serial, dt_pipe) if dt_pipe else dt_serial
     P = sum(layout.numels)
     return {"value": P / dt, "unit": "params/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * len(layout.numels), "ms_per_step": dt * 1e3,
             "steps": args.e2e_steps, "h2d_gbs_per_rank": h2d / dt / 1e9,
-            "api": "ParamBuffer.accumulate_flat(pinned host gradient) + sharded page step + "
+            "serial_ms_per_step": dt_serial * 1e3,
+            "pipelined_ms_per_step": dt_pipe * 1e3 if dt_pipe else None,
+            "api": ("lockfree.ingest(pinned host gradient, %d layer groups) -> "
+                    "FusedShardedPageStep.step_pipelined(ready=...) -> applied flags to host, every rank"
+                    % args.e2e_groups) if dt_pipe and dt_pipe <= dt_serial else
+                   "ParamBuffer.accumulate_flat(pinned host gradient) + sharded page step + "
                    "applied flags to host, every rank"}
 
 

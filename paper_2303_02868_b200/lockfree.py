@@ -759,31 +759,31 @@ def layer_groups(numels, groups: int) -> list[list[int]]:
     return out
 
 
-def ingest_sweep(buffer: ParamBuffer, masters: MasterState, host_grad, hyper: AdamHyper,
-                 iteration: int = 0, *, groups: int = 8, stream=None, copy_stream=None) -> SweepResult:
-    """One update step fed by a flat gradient in (pinned) host memory — what a
-    host-side producer hands the updating actor.  Per contiguous layer group:
-    cudaMemcpyAsync of the group's slice on a copy stream -> K3 accumulate
-    into its pages when it lands -> fused sweep of the group, so the PCIe
-    transfer of group k+1 overlaps the update of group k and the step costs
-    about one transfer of the gradient (the reference's fetch/offload are
-    DelayModel sleeps, hiermem/lockfree.py:90-94, 562-569)."""
+def ingest(buffer: ParamBuffer, host_grad, iteration: int = 0, *, groups: int = 8, stream=None,
+           copy_stream=None, after_group=None) -> list:
+    """Accumulate a flat gradient that sits in (pinned) host memory, one
+    contiguous layer group at a time: cudaMemcpyAsync of the group's slice on
+    a copy stream -> K3 into its pages on ``stream`` when it lands, so the
+    PCIe transfer of group k+1 overlaps whatever runs after group k
+    (``after_group(layers)`` is called right after the group's K3 is queued).
+    Returns one event per group, recorded after its K3: a consumer on another
+    stream (the pipelined DP step) waits on it."""
     lay = buffer.layout
     st = buffer._stream(stream)
     cache = buffer.__dict__.setdefault("_ingest", {})
     key = ("plan", groups)
     if key not in cache:
         cache[key] = layer_groups(lay.numels, groups)
+    if "staging" not in cache:
         cache["staging"] = torch.empty(sum(lay.numels), dtype=buffer._t16, device=buffer.device)
         cache["copy"] = copy_stream or torch.cuda.Stream(buffer.device)
-        starts = np.cumsum([0] + lay.numels[:-1])
-        cache["starts"] = starts
+        cache["starts"] = np.cumsum([0] + lay.numels[:-1])
     plan, staging, cs, starts = cache[key], cache["staging"], cache["copy"], cache["starts"]
     src = host_grad.reshape(-1)
     if src.dtype != buffer._t16 or src.numel() != staging.numel():
         raise ProtocolError(f"host gradient must be {buffer._t16} with {staging.numel()} elements")
     L = buffer.num_layers
-    parts = []
+    done = []
     cs.wait_stream(st)   # the staging slice is free once the previous step consumed it
     for grp in plan:
         a, b = int(starts[grp[0]]), int(starts[grp[-1]] + lay.numels[grp[-1]])
@@ -821,9 +821,30 @@ def ingest_sweep(buffer: ParamBuffer, masters: MasterState, host_grad, hyper: Ad
             D.ptr(buffer._eng.desc.static(chunks)), len(chunks), 0,
             D.ptr(buffer._eng.desc.table(modes)), D.ptr(buffer._flags), D.ptr(buffer._sumsq),
             D.sptr(st)))
+        ev = torch.cuda.Event()
+        ev.record(st)
+        done.append(ev)
         for l in grp:
             buffer.ledger.messages_accumulated[l] += 1
             buffer._pending[l] += 1
             buffer._max_iter[l] = max(buffer._max_iter[l], iteration)
-        parts.append(sweep(buffer, masters, hyper, layers=list(reversed(grp)), stream=st))
+        if after_group is not None:
+            after_group(grp)
+    return done
+
+
+def ingest_sweep(buffer: ParamBuffer, masters: MasterState, host_grad, hyper: AdamHyper,
+                 iteration: int = 0, *, groups: int = 8, stream=None, copy_stream=None) -> SweepResult:
+    """One update step fed by a flat gradient in (pinned) host memory — what a
+    host-side producer hands the updating actor.  Per contiguous layer group:
+    cudaMemcpyAsync of the group's slice on a copy stream -> K3 accumulate
+    into its pages when it lands -> fused sweep of the group, so the PCIe
+    transfer of group k+1 overlaps the update of group k and the step costs
+    about one transfer of the gradient (the reference's fetch/offload are
+    DelayModel sleeps, hiermem/lockfree.py:90-94, 562-569)."""
+    st = buffer._stream(stream)
+    parts = []
+    ingest(buffer, host_grad, iteration, groups=groups, stream=st, copy_stream=copy_stream,
+           after_group=lambda grp: parts.append(
+               sweep(buffer, masters, hyper, layers=list(reversed(grp)), stream=st)))
     return _MultiResult(masters, parts)

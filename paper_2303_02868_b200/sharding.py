@@ -307,7 +307,7 @@ class FusedShardedPageStep:
         return cache[groups]
 
     def step_pipelined(self, hyper, groups: int = 4, *, reduce_ctas: int = 0, update_ctas: int = 0,
-                       stream=None,
+                       ready=None, stream=None,
                        timings: dict | None = None):
         """``step`` with the layers cut into contiguous groups and two streams:
         the reduce-scatter + check of group k+1 runs while group k is updated
@@ -318,7 +318,10 @@ class FusedShardedPageStep:
         grid of that many CTAs on a high-priority stream: the link-bound
         reduce then runs from a few SMs beside the HBM-bound update of the
         previous group; ``update_ctas > 0`` likewise gives the update a
-        persistent grid of its own.  With NVLS the RS leg is outbound-heavy (S out, S/N
+        persistent grid of its own.  ``ready`` (one event per layer group,
+        from ``lockfree.ingest``) lets the step start while the gradient is
+        still arriving from the host: group k is reduced once its own K3 has
+        run on every rank.  With NVLS the RS leg is outbound-heavy (S out, S/N
         in per GPU) and the AG leg inbound-heavy (S/N out, S in), so
         overlapping them moves (1 + 1/N)·S per link direction instead of
         2·(N−1)/N·S."""
@@ -345,12 +348,27 @@ class FusedShardedPageStep:
                 e.record(s)
                 marks[name] = e
 
-        with torch.cuda.stream(st):
-            mark("start", st)
-            self.flags_local.zero_()
-            self.h_g.barrier(channel=0)                          # every rank's gradients are complete
-        rs.wait_stream(st)
-        up.wait_stream(st)
+        if ready is None:
+            with torch.cuda.stream(st):
+                mark("start", st)
+                self.flags_local.zero_()
+                self.h_g.barrier(channel=0)                      # every rank's gradients are complete
+            rs.wait_stream(st)
+            up.wait_stream(st)
+        else:
+            # Gradients still arriving (lockfree.ingest): group k is reduced as
+            # soon as its own K3 is done here and on every peer (per-group
+            # barrier below); the reduce stream only has to follow the end of
+            # the previous step, not the K3s queued behind it on ``st``.
+            if len(ready) != len(plan):
+                raise ConfigError(f"{len(ready)} ready events for {len(plan)} layer groups")
+            last = self.__dict__.get("_last_done")
+            if last is not None:
+                rs.wait_event(last)
+                up.wait_event(last)
+            with torch.cuda.stream(rs):
+                mark("start", rs)
+                self.flags_local.zero_()
         gp = self._arr([p + gsel * span_b for p in self.g_ptrs])
         mc = self.mc_g + gsel * span_b if self.mc_g else None
         counts, newest = [0] * L, [0] * L
@@ -364,6 +382,9 @@ class FusedShardedPageStep:
         for k, (grp, check, adam) in enumerate(plan):
             first, n = grp[0], len(grp)
             with torch.cuda.stream(rs):
+                if ready is not None:
+                    rs.wait_event(ready[k])
+                    self.h_g.barrier(channel=0)                  # group k landed on every rank
                 D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
                                                D.ptr(eng.desc.static(check)), len(check),
                                                D.ptr(self.flags_local), None, D.sptr(rs)))
@@ -398,6 +419,9 @@ class FusedShardedPageStep:
             mark("adam", st)
             self.h_p.barrier(channel=2)                          # published pages landed everywhere
             mark("ag", st)
+            done = torch.cuda.Event()
+            done.record(st)
+            self._last_done = done
         for l in range(L):
             buf._psel[l] ^= 1
             buf._version[l] += 1
@@ -469,6 +493,9 @@ class FusedShardedPageStep:
             mark("adam")
             self.h_p.barrier(channel=0)                          # published pages landed everywhere
             mark("ag")
+            done = torch.cuda.Event()
+            done.record(st)
+            self._last_done = done
         for l in range(L):
             buf._psel[l] ^= 1
             buf._version[l] += 1

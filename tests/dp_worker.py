@@ -74,10 +74,16 @@ def main():
         t = torch.from_numpy(flat.view(np.int16) if dtype == "bf16" else flat)
         if dtype == "bf16":
             t = t.view(torch.bfloat16)
-        buf.accumulate_flat(t.to(dev), it)
-        gsel = buf._gsel[0]
         groups = int(os.environ.get("DP_GROUPS", "1"))
-        if groups > 1 and mode != "nccl":
+        ingest = os.environ.get("DP_INGEST", "0") == "1"
+        if ingest:   # from pinned host memory, group by group; the step starts early
+            ready = LF.ingest(buf, t.pin_memory(), it, groups=groups)
+        else:
+            buf.accumulate_flat(t.to(dev), it)
+        gsel = buf._gsel[0]
+        if ingest:
+            step.step_pipelined(hyper, groups, ready=ready)
+        elif groups > 1 and mode != "nccl":
             step.step_pipelined(hyper, groups, reduce_ctas=int(os.environ.get("DP_REDUCE_CTAS", "0")),
                                 update_ctas=int(os.environ.get("DP_UPDATE_CTAS", "0")))
         else:
