@@ -220,6 +220,8 @@ def run_ours_single(args):
     from paper_2303_02868_b200 import lockfree as LF
     from paper_2303_02868_b200 import workloads as W
     device = torch.device("cuda", 0)
+    from paper_2303_02868_b200 import _device as Dv
+    numa = Dv.bind_to_gpu_numa(0)   # pinned host buffers next to the GPU's PCIe root
     torch.cuda.set_device(device)
     specs, page, layout, buf, ms = build_state(args, device)
     L = len(specs)
@@ -286,6 +288,7 @@ def run_ours_single(args):
     e2e = run_e2e(args, buf, ms, hyper, grads, device) if args.e2e_steps > 0 else None
     traffic = load_traffic(args)
     cpu = None
+    Dv.restore_affinity(numa)   # the CPU baseline gets every host core
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n, t = cpu_reference_sample(specs, page, args.cpu_sample_pages, threads, args.dtype, reps=2)
@@ -301,6 +304,7 @@ def run_ours_single(args):
                    "layers": L, "page_bytes": page, "pages": layout.used_pages,
                    "adam_threads": args.adam_threads,
                    "adam_variant": ["ldg", "tma"][args.adam_variant],
+                   "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
                    "l2": "inputs larger than L2 (28 B/param x params >> 126 MB)",
                    "step": "fused sweep: prologue + page-Adam over all pages (take->update->publish)"},
         "hbm_gbs": achieved,

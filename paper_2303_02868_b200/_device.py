@@ -210,3 +210,48 @@ def to_host(t: torch.Tensor, shape, readonly: bool = False) -> np.ndarray:
 
 def check(rc: int) -> None:
     N.check(rc)
+
+
+def _parse_cpulist(text: str) -> set[int]:
+    cpus = set()
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        lo, _, hi = part.partition("-")
+        cpus.update(range(int(lo), int(hi or lo) + 1))
+    return cpus
+
+
+def bind_to_gpu_numa(device_index: int) -> dict | None:
+    """Pin the calling process to the CPUs of the NUMA node that hosts the
+    GPU's PCIe root, so pinned host buffers allocated afterwards (first touch)
+    live next to that GPU's link — with one rank per GPU, every rank's
+    host->device stream then stays on its own socket.  No-op (None) when the
+    topology is not visible, the node is unknown, or HM_NO_NUMA_BIND=1."""
+    import os
+    if os.environ.get("HM_NO_NUMA_BIND") == "1" or not hasattr(os, "sched_setaffinity"):
+        return None
+    try:
+        p = torch.cuda.get_device_properties(device_index)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+            node = int(f.read().strip())
+        if node < 0:
+            return None
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            cpus = _parse_cpulist(f.read()) & os.sched_getaffinity(0)
+        if not cpus:
+            return None
+        before = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, cpus)
+        return {"numa_node": node, "cpus": len(cpus), "pci": bus, "_before": sorted(before)}
+    except (OSError, ValueError, AttributeError, RuntimeError):
+        return None
+
+
+def restore_affinity(info: dict | None) -> None:
+    """Undo bind_to_gpu_numa (e.g. before a CPU-side measurement that should
+    use every host core)."""
+    import os
+    if info and info.get("_before"):
+        os.sched_setaffinity(0, set(info["_before"]))

@@ -65,6 +65,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     from . import workloads as W
     from .sharding import FusedShardedPageStep, ShardedPageStep, symmetric_alloc
     rank, world, device = _init()
+    from . import _device as Dv
+    numa = Dv.bind_to_gpu_numa(device.index)   # this rank's pinned buffers next to its GPU
     fused = args.dp_mode != "nccl"
     fallback = None
     if fused:
@@ -191,6 +193,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": P, "layers": L,
                    "page_bytes": page, "pages": layout.used_pages, "bucket_pages_per_rank": layout.K,
                    "buckets": layout.num_buckets, "parallelism": f"dp{world} (page-sharded ZeRO-3)",
+                   "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
                    "l2": "inputs larger than L2",
                    "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
                    "dp_groups": args.dp_groups if pipelined else 1,

@@ -76,3 +76,9 @@ def test_null_pointers_rejected_before_launch():
     assert lib.hm_set_dp_reduce_ctas(-1) == INVALID and lib.hm_set_dp_reduce_ctas(0) == 0
     assert lib.hm_set_ag_publish(3) == INVALID and lib.hm_set_ag_publish(0) == 0
     assert lib.hm_set_adam_threads(300) == INVALID
+
+
+def test_cpulist_parser():
+    from paper_2303_02868_b200._device import _parse_cpulist
+    assert _parse_cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert _parse_cpulist("") == set()
