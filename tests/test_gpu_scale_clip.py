@@ -1,0 +1,104 @@
+"""Gradient unscale and global grad-norm clipping in the fused page-Adam
+(north star: "gradient unscale ... using warp-level reductions for the
+overflow/grad-norm checks").  The reference has neither (its AdamHyper is
+lr/betas/eps, hiermem/lockfree.py:37-42), so the oracle is the reference
+chain fed the scaled gradient:  g' = f32(f32(g16) * gscale)  with
+
+    gscale = f32(inv_scale)                                  (no clipping)
+    gscale = f32(inv_scale) * f32(coef),  coef = max_norm / (norm + 1e-6)
+             if norm = sqrt(sum_l sum g^2) * inv_scale > max_norm   (clipping)
+
+summed over the layers that are not rejected.  Unscale alone is bit-exact.
+With clipping the device sums the squares per CTA in f32 before the f64
+total, so coef can differ from the exact one in its last bit: masters are
+checked to 1e-6 relative (the north star's master tolerance) and coef to
+1e-6 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import page_adam as O
+from paper_2303_02868_b200 import lockfree as LF
+
+pytestmark = pytest.mark.gpu
+SIZES = [70001, 5, 40000, 777, 65539, 4096 * 9 + 3]
+
+
+def bits(x):
+    x = np.asarray(x)
+    return x.view(np.uint32) if x.dtype == np.float32 else x.view(np.uint16)
+
+
+def run(dtype, hyper, grad_scale, nan_layer=None, seed=3):
+    rng = np.random.default_rng(seed)
+    params = [rng.normal(0, 0.02, n).astype(np.float32) for n in SIZES]
+    buf = LF.ParamBuffer(params, dtype=dtype, page_bytes=64 * 1024)
+    ms = LF.MasterState(params, page_bytes=64 * 1024)
+    grads = []
+    for l, n in enumerate(SIZES):
+        g = rng.normal(0, 1e-2, n).astype(np.float32) * np.float32(grad_scale)
+        if l == nan_layer:
+            g[n // 3] = np.inf
+        g16 = O.to16(g, dtype)
+        grads.append(g16)
+        payload = g16 if dtype == "fp16" else torch.from_numpy(g16.view(np.int16)).view(torch.bfloat16)
+        buf.accumulate(LF.GradMessage(l, payload, 0))
+    applied = LF.sweep(buf, ms, hyper).applied()
+    return params, grads, buf, ms, applied
+
+
+def oracle(params, grads, dtype, gscale, lr):
+    om = O.OracleMasters(params)
+    ok = []
+    for l, g16 in enumerate(grads):
+        g = O.from16(g16, dtype)
+        ok.append(om.update_layer(l, (g * np.float32(gscale)).astype(np.float32), lr=lr))
+    return om, ok
+
+
+@pytest.mark.parametrize("dtype,inv_scale,grad_scale", [("fp16", 1 / 1024, 1024.0),
+                                                        ("bf16", 0.25, 4.0), ("fp16", 1.0, 1.0)])
+def test_unscale_bit_exact(cuda, dtype, inv_scale, grad_scale):
+    hyper = LF.AdamHyper(lr=1e-3, inv_scale=inv_scale)
+    params, grads, buf, ms, applied = run(dtype, hyper, grad_scale, nan_layer=2)
+    om, ok = oracle(params, grads, dtype, np.float32(inv_scale), 1e-3)
+    assert [applied[l] for l in range(len(SIZES))] == ok and not ok[2]
+    for l in range(len(SIZES)):
+        np.testing.assert_array_equal(bits(ms.p32[l]), bits(om.p32[l]), err_msg=f"p32 {l}")
+        np.testing.assert_array_equal(bits(ms.m32[l]), bits(om.m32[l]), err_msg=f"m32 {l}")
+        np.testing.assert_array_equal(bits(ms.v32[l]), bits(om.v32[l]), err_msg=f"v32 {l}")
+        pub = buf.read(l)[1]
+        pub = bits(pub) if dtype == "fp16" else np.asarray(pub).view(np.uint16)
+        np.testing.assert_array_equal(pub, bits(O.publish16(om.p32[l], dtype)), err_msg=f"p16 {l}")
+
+
+@pytest.mark.parametrize("max_norm,expect_clip", [(0.05, True), (1e6, False)])
+def test_global_norm_clip(cuda, max_norm, expect_clip):
+    dtype, inv_scale = "bf16", 0.5
+    hyper = LF.AdamHyper(lr=1e-3, inv_scale=inv_scale, max_norm=max_norm)
+    params, grads, buf, ms, applied = run(dtype, hyper, 2.0, nan_layer=4)
+    # exact global norm over the layers that are applied (layer 4 is rejected)
+    total = sum(float(np.sum(O.from16(g, dtype).astype(np.float64) ** 2))
+                for l, g in enumerate(grads) if l != 4)
+    norm = np.sqrt(total) * inv_scale
+    coef = max_norm / (norm + 1e-6) if norm > max_norm else 1.0
+    assert (norm > max_norm) == expect_clip
+    gscale = np.float32(np.float32(inv_scale) * np.float32(coef))
+    om, ok = oracle(params, grads, dtype, gscale, 1e-3)
+    assert [applied[l] for l in range(len(SIZES))] == ok and not ok[4]
+    for l in range(len(SIZES)):
+        for got, want, name in ((ms.p32[l], om.p32[l], "p32"), (ms.m32[l], om.m32[l], "m32"),
+                                (ms.v32[l], om.v32[l], "v32")):
+            got = np.asarray(got.cpu() if isinstance(got, torch.Tensor) else got)
+            np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-12, err_msg=f"{name} {l}")
+        if not expect_clip:   # coef == 1 exactly: the unscale path, bit-exact
+            np.testing.assert_array_equal(bits(ms.p32[l]), bits(om.p32[l]))
+    if expect_clip:
+        # the update really shrank: |m| ~ (1 - beta1) * |g * gscale|, check the ratio
+        l = 0
+        g = O.from16(grads[l], dtype)
+        m = np.asarray(ms.m32[l].cpu() if isinstance(ms.m32[l], torch.Tensor) else ms.m32[l])
+        nz = g != 0
+        ratio = np.median(m[nz] / (np.float32(0.1) * g[nz]))
+        assert ratio == pytest.approx(gscale, rel=1e-5)
