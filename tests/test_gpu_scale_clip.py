@@ -88,10 +88,13 @@ def test_global_norm_clip(cuda, max_norm, expect_clip):
     om, ok = oracle(params, grads, dtype, gscale, 1e-3)
     assert [applied[l] for l in range(len(SIZES))] == ok and not ok[4]
     for l in range(len(SIZES)):
-        for got, want, name in ((ms.p32[l], om.p32[l], "p32"), (ms.m32[l], om.m32[l], "m32"),
-                                (ms.v32[l], om.v32[l], "v32")):
+        # 1e-6 relative; p32 gets an absolute floor of 1e-6 x lr for masters that
+        # sit near zero (a last-bit change of coef moves p by ~1e-7 of its step)
+        for got, want, name, atol in ((ms.p32[l], om.p32[l], "p32", 1e-6 * 1e-3),
+                                      (ms.m32[l], om.m32[l], "m32", 0.0),
+                                      (ms.v32[l], om.v32[l], "v32", 0.0)):
             got = np.asarray(got.cpu() if isinstance(got, torch.Tensor) else got)
-            np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-12, err_msg=f"{name} {l}")
+            np.testing.assert_allclose(got, want, rtol=1e-6, atol=atol, err_msg=f"{name} {l}")
         if not expect_clip:   # coef == 1 exactly: the unscale path, bit-exact
             np.testing.assert_array_equal(bits(ms.p32[l]), bits(om.p32[l]))
     if expect_clip:
