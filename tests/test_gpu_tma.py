@@ -1,5 +1,6 @@
 """The TMA bulk-copy variant of the page-Adam main pass (page_adam_tma.cu,
-hm_set_adam_variant(1)) produces the same bits as the oracle on every path:
+hm_set_adam_variant(1)) — and the 512-thread form of the LDG kernel — produce
+the same bits as the oracle on every path:
 aligned chunks through the shared-memory pipeline, unaligned heads/tails from
 global memory, rejected layers (publish only), f32 gradients (apply_update)."""
 import numpy as np
@@ -22,8 +23,25 @@ def tma_variant():
     N.check(N.lib().hm_set_adam_variant(0))
 
 
+@pytest.fixture()
+def threads512():
+    N.check(N.lib().hm_set_adam_threads(512))
+    yield
+    N.check(N.lib().hm_set_adam_threads(256))
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 def test_tma_sweep_bit_exact(cuda, tma_variant, dtype):
+    _sweep_bit_exact(dtype)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_512_thread_variant_bit_exact(cuda, threads512, dtype):
+    """hm_set_adam_threads(512): one granule per thread instead of two."""
+    _sweep_bit_exact(dtype)
+
+
+def _sweep_bit_exact(dtype):
     rng = np.random.default_rng(17)
     params = [rng.normal(0, 0.02, n).astype(np.float32) for n in SIZES]
     buf = LF.ParamBuffer(params, dtype=dtype, page_bytes=64 * 1024)
