@@ -17,10 +17,16 @@ HBM byte buffer and whose CPU pool is a pinned host byte buffer:
 * ``tensor_merge`` copies every relocated chunk (keeping its in-page offset)
   through a staging buffer, so chains like page 5 -> 3 while 3 -> 4 are safe.
 
-SSD pools stay metadata-only (no GDS in the image); touching their bytes
-raises ConfigError.
+An SSD pool is backed by a file when ``ssd_path`` is given (no GPUDirect
+Storage in the image: POSIX I/O from the host, ``O_DIRECT`` when the
+filesystem allows it, through a pinned page-sized bounce buffer for the GPU
+side); page moves to and from it and pack/unpack of SSD-resident pages move
+real bytes.  Without ``ssd_path`` the SSD pool stays metadata-only, as in
+the reference, and touching its bytes raises ConfigError.
 """
 from __future__ import annotations
+
+import os
 
 import numpy as np
 import torch
@@ -46,23 +52,88 @@ def _descs(rows) -> np.ndarray:
 
 
 class DevicePageManager(PageManager):
-    def __init__(self, pool_specs, device=None):
+    def __init__(self, pool_specs, device=None, *, ssd_path: str | None = None):
         super().__init__(pool_specs)
         self.device = D.require_device(device)
         self.copy_stream = torch.cuda.Stream(self.device)
-        self.storage: dict[Tier, torch.Tensor] = {}
+        self.storage: dict[Tier, torch.Tensor | None] = {}
+        self._fd = None
         for tier, pool in self.pools.items():
             if tier is Tier.GPU:
                 self.storage[tier] = torch.zeros(pool.capacity_bytes, dtype=torch.uint8, device=self.device)
             elif tier is Tier.CPU:
                 self.storage[tier] = torch.zeros(pool.capacity_bytes, dtype=torch.uint8, pin_memory=True)
+            elif tier is Tier.SSD and ssd_path is not None:
+                from .ssd import _open
+                self._fd, self.ssd_direct = _open(ssd_path, direct=True)
+                os.ftruncate(self._fd, pool.capacity_bytes)
+                self._ssd_page = pool.page_bytes
+                self._bounce = torch.empty(pool.page_bytes, dtype=torch.uint8, pin_memory=True)
+                self.storage[tier] = None          # backed by the file, not a tensor
+
+    def close(self) -> None:
+        if self._fd is not None:
+            os.close(self._fd)
+            self._fd = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the SSD file (whole pages: O_DIRECT needs aligned offsets and sizes) ----
+    def _pread(self, off: int, buf: torch.Tensor) -> None:
+        mv = memoryview(buf.numpy()).cast("B")
+        done = 0
+        while done < len(mv):
+            n = os.preadv(self._fd, [mv[done:]], off + done)
+            if n <= 0:
+                raise OSError(f"short read from the SSD pool at {off + done}")
+            done += n
+
+    def _pwrite(self, off: int, buf: torch.Tensor) -> None:
+        mv = memoryview(buf.numpy()).cast("B")
+        done = 0
+        while done < len(mv):
+            n = os.pwritev(self._fd, [mv[done:]], off + done)
+            if n <= 0:
+                raise OSError(f"short write to the SSD pool at {off + done}")
+            done += n
+
+    def _ssd_read_bytes(self, addr: int, n: int) -> np.ndarray:
+        """Bytes [addr, addr+n) of the SSD pool (read page by page)."""
+        P = self._ssd_page
+        out = np.empty(n, dtype=np.uint8)
+        pos = 0
+        while pos < n:
+            base = (addr + pos) // P * P
+            k = min(n - pos, base + P - (addr + pos))
+            self._pread(base, self._bounce)
+            lo = addr + pos - base
+            out[pos:pos + k] = self._bounce.numpy()[lo:lo + k]
+            pos += k
+        return out
+
+    def _ssd_write_bytes(self, addr: int, data: np.ndarray) -> None:
+        """Read-modify-write of whole pages (partial runs keep their neighbours)."""
+        P, n, pos = self._ssd_page, len(data), 0
+        while pos < n:
+            base = (addr + pos) // P * P
+            k = min(n - pos, base + P - (addr + pos))
+            lo = addr + pos - base
+            if k < P:
+                self._pread(base, self._bounce)
+            self._bounce.numpy()[lo:lo + k] = data[pos:pos + k]
+            self._pwrite(base, self._bounce)
+            pos += k
 
     # -- addressing -----------------------------------------------------------
     def _loc(self, pid: int):
         for tier, pool in self.pools.items():
             if pid in pool.pages:
                 if tier not in self.storage:
-                    raise ConfigError(f"{tier.name} pages have no backing store here (no GDS)")
+                    raise ConfigError(f"{tier.name} pages have no backing store (pass ssd_path= to back the SSD pool)")
                 return tier, (pid - pool.first_page_id) * pool.page_bytes
         raise KeyError(f"unknown page id {pid}")
 
@@ -95,6 +166,11 @@ class DevicePageManager(PageManager):
                 D.check(lib.hm_copy_runs(D.ptr(dev), D.ptr(store), D.ptr(self._up(d)), len(d), D.sptr(st)))
                 if dev is not raw:
                     dev.record_stream(st)
+            elif tier is Tier.SSD:
+                st.synchronize()
+                host = raw.cpu().numpy()
+                for sp, dpos, n in rows:
+                    self._ssd_write_bytes(dpos, host[sp:sp + n])
             else:
                 kind = 2 if raw.is_cuda else 0
                 if kind == 0:
@@ -119,6 +195,11 @@ class DevicePageManager(PageManager):
             if tier is Tier.GPU:
                 d = _descs(inv)
                 D.check(lib.hm_copy_runs(D.ptr(store), D.ptr(out), D.ptr(self._up(d)), len(d), D.sptr(st)))
+            elif tier is Tier.SSD:
+                for src, dst, n in inv:
+                    chunk = torch.from_numpy(self._ssd_read_bytes(src, n))
+                    with torch.cuda.stream(st):
+                        out[dst:dst + n].copy_(chunk)
             else:
                 d = np.array(inv, dtype=N.COPY_DESC)
                 D.check(lib.hm_memcpy_runs(D.ptr(store), D.ptr(out), d.ctypes.data, len(d), 1, D.sptr(st)))
@@ -137,21 +218,48 @@ class DevicePageManager(PageManager):
         raise KeyError(f"unknown page id {pid}")
 
     def page_move(self, page_id: int, target_tier, *, stream=None) -> TransferDescriptor:
-        backed_src = self._tier_of(page_id) in self.storage
-        src_off = self._loc(page_id)[1] if backed_src else None
         src_tier = self._tier_of(page_id)
+        backed_src = src_tier in self.storage
+        src_off = self._loc(page_id)[1] if backed_src else None
         desc = super().page_move(page_id, target_tier)
         if not backed_src or desc.dst_tier not in self.storage:
-            return desc  # an SSD side is metadata-only, as in the reference
+            return desc  # an unbacked SSD side is metadata-only, as in the reference
         dst_tier, dst_off = self._loc(desc.new_page_id)
         st = D.cur_stream(self.device, stream)
         self.copy_stream.wait_stream(st)
+        n = desc.bytes
+        if Tier.SSD in (src_tier, dst_tier):
+            self._move_ssd(src_tier, src_off, dst_tier, dst_off, n)
+            return desc
         kind = {(Tier.GPU, Tier.CPU): 2, (Tier.CPU, Tier.GPU): 1}[(src_tier, dst_tier)]
-        d = np.array([(src_off, dst_off, desc.bytes)], dtype=N.COPY_DESC)
+        d = np.array([(src_off, dst_off, n)], dtype=N.COPY_DESC)
         D.check(N.lib().hm_memcpy_runs(D.ptr(self.storage[src_tier]), D.ptr(self.storage[dst_tier]),
                                        d.ctypes.data, 1, kind, D.sptr(self.copy_stream)))
         st.wait_stream(self.copy_stream)
         return desc
+
+    def _move_ssd(self, src_tier, src_off, dst_tier, dst_off, n) -> None:
+        """Whole-page moves to / from the SSD file (synchronous: the bounce
+        buffer and the CPU pool are host memory the I/O reads directly)."""
+        cs = self.copy_stream
+        if src_tier is Tier.GPU:        # GPU -> SSD: D2H into the bounce, then write
+            d = np.array([(src_off, 0, n)], dtype=N.COPY_DESC)
+            D.check(N.lib().hm_memcpy_runs(D.ptr(self.storage[Tier.GPU]), D.ptr(self._bounce),
+                                           d.ctypes.data, 1, 2, D.sptr(cs)))
+            cs.synchronize()
+            self._pwrite(dst_off, self._bounce[:n])
+        elif dst_tier is Tier.GPU:      # SSD -> GPU: read into the bounce, then H2D
+            self._pread(src_off, self._bounce[:n])
+            d = np.array([(0, dst_off, n)], dtype=N.COPY_DESC)
+            D.check(N.lib().hm_memcpy_runs(D.ptr(self._bounce), D.ptr(self.storage[Tier.GPU]),
+                                           d.ctypes.data, 1, 1, D.sptr(cs)))
+            cs.synchronize()
+        elif src_tier is Tier.CPU:      # CPU -> SSD straight from the pinned pool
+            cs.synchronize()
+            self._pwrite(dst_off, self.storage[Tier.CPU][src_off:src_off + n])
+        else:                           # SSD -> CPU straight into the pinned pool
+            cs.synchronize()
+            self._pread(src_off, self.storage[Tier.CPU][dst_off:dst_off + n])
 
     def tensor_merge(self, tensor_id: int, *, stream=None) -> dict:
         t = self.tensors.get(tensor_id)
@@ -182,6 +290,10 @@ class DevicePageManager(PageManager):
             g, s = _descs(gather), _descs(scatter)
             D.check(N.lib().hm_copy_runs(D.ptr(store), D.ptr(tmp), D.ptr(self._up(g)), len(g), D.sptr(st)))
             D.check(N.lib().hm_copy_runs(D.ptr(tmp), D.ptr(store), D.ptr(self._up(s)), len(s), D.sptr(st)))
+        elif tier is Tier.SSD:
+            tmp = [self._ssd_read_bytes(a0, n) for a0, _, n in moves]   # gather first: chains
+            for (a0, a1, n), buf in zip(moves, tmp):
+                self._ssd_write_bytes(a1, buf)
         else:
             st.synchronize()
             tmp = [store[a0:a0 + n].clone() for a0, _, n in moves]

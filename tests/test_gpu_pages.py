@@ -115,3 +115,54 @@ def test_pack_matches_oracle_layout(cuda):
         O.pack(pool, d, t.segments(), PAGE // 2, 2)
     got = dm.storage[next(iter(dm.storage))].cpu().numpy().view(np.uint16)
     assert np.array_equal(got, pool)
+
+
+def test_ssd_tier_moves_bytes(cuda, tmp_path):
+    """An SSD pool backed by a file: page_move GPU/CPU <-> SSD (fp32 pages
+    only, the reference's rule), pack/unpack of SSD-resident pages and a merge
+    inside the SSD tier all move real bytes; the page table stays identical
+    to the metadata-only manager."""
+    specs = [("GPU", 16 * PAGE, PAGE), ("CPU", 16 * PAGE, PAGE), ("SSD", 16 * PAGE, PAGE)]
+    dm = DevicePageManager(specs, ssd_path=str(tmp_path / "ssd.pool"))
+    meta = PageManager(specs)
+    nrng = np.random.default_rng(7)
+    nbytes = 3 * PAGE + 4096
+    spec = TensorSpec("opt", "optim32", nbytes, 0)
+    t = dm.allocate(spec, "GPU")
+    meta.allocate(spec, "GPU")
+    data = nrng.normal(0, 1, nbytes // 4).astype(np.float32)
+    dm.write(t.tensor_id, data)
+
+    def check(want):
+        got = dm.read(t.tensor_id).cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+    for pid in list(dm.tensors[t.tensor_id].page_list):          # GPU -> SSD
+        assert dm.page_move(pid, "SSD") == meta.page_move(pid, "SSD")
+        check(data)
+    data2 = nrng.normal(0, 1, nbytes // 4).astype(np.float32)     # pack into SSD pages
+    dm.write(t.tensor_id, torch.from_numpy(data2).cuda())
+    check(data2)
+    for hop in ("CPU", "SSD", "GPU"):                             # SSD -> CPU -> SSD -> GPU
+        for pid in list(dm.tensors[t.tensor_id].page_list):
+            assert dm.page_move(pid, hop) == meta.page_move(pid, hop)
+        check(data2)
+    # a 16-bit tensor may not go to SSD (hiermem/pagemem.py page_move rules)
+    h = dm.allocate(TensorSpec("p16", "param16", PAGE, 0), "GPU")
+    meta.allocate(TensorSpec("p16", "param16", PAGE, 0), "GPU")
+    with pytest.raises(MoveError):
+        dm.page_move(dm.tensors[h.tensor_id].page_list[0], "SSD")
+    with pytest.raises(MoveError):
+        meta.page_move(meta.tensors[h.tensor_id].page_list[0], "SSD")
+    # merge inside the SSD tier: fragment, then defragment with data
+    for pid in list(dm.tensors[t.tensor_id].page_list):
+        dm.page_move(pid, "SSD")
+        meta.page_move(pid, "SSD")
+    a = dm.allocate(TensorSpec("gap", "optim32", PAGE, 0), "SSD")
+    meta.allocate(TensorSpec("gap", "optim32", PAGE, 0), "SSD")
+    dm.release(a.tensor_id)
+    meta.release(a.tensor_id)
+    assert dm.tensor_merge(t.tensor_id) == meta.tensor_merge(t.tensor_id)
+    check(data2)
+    assert dm.state_dict() == meta.state_dict()
+    dm.close()
