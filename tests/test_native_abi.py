@@ -82,3 +82,16 @@ def test_cpulist_parser():
     from paper_2303_02868_b200._device import _parse_cpulist
     assert _parse_cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
     assert _parse_cpulist("") == set()
+
+
+def test_ctypes_arity_matches_header():
+    """Every prototype's parameter count equals the ctypes argtypes length (a
+    missing argument would shift every later one at the call site)."""
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "hm_page.h").read_text(), flags=re.S)
+    protos = re.findall(r"\b(?:int|int64_t|const char\s*\*|void|uint32_t)\s+\**\s*(hm_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;",
+                        text, flags=re.S)
+    assert {p[0] for p in protos} == declared_functions()
+    for name, params in protos:
+        params = params.strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        assert n == len(N.SIGNATURES[name][1]), f"{name}: header {n} params, ctypes {len(N.SIGNATURES[name][1])}"
