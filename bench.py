@@ -408,6 +408,10 @@ def main():
     ap.add_argument("--cpu-sample-pages", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c3-layers", type=int, default=8, help="C3 slice (host-memory bound)")
+    ap.add_argument("--c3-lockfree-iters", type=int, default=4,
+                    help="C3 host tier: also time sync vs lock-free delayed update (0 = skip)")
+    ap.add_argument("--c3-tokens", type=int, default=16384,
+                    help="tokens per step of the modelled GPU actor (C3 lock-free line)")
     ap.add_argument("--adam-threads", type=int, default=256, choices=[256, 512])
     ap.add_argument("--adam-variant", type=int, default=0, choices=[0, 1],
                     help="page-Adam data movement: 0 LDG/STG streaming, 1 TMA bulk-copy pipeline")

@@ -166,6 +166,9 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
         roof = {"bound": "pcie", "achieved": achieved, "peak": pcie["bidir_gbs"], "unit": "GB/s",
                 "frac": achieved / pcie["bidir_gbs"], "peak_kind": "measured pinned cudaMemcpyAsync "
                 "H2D||D2H on this box", "bytes_per_param": 24, "pcie": pcie}
+    lockfree = None
+    if args.state_tier == "host" and args.c3_lockfree_iters > 0:
+        lockfree = _lockfree(args, buf, hm, hyper, grads, P, device)
     line = {
         "metric": metric, "value": P / (ms_step / 1e3), "unit": "params/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -180,4 +183,40 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
         "clocks": clk.summary(),
         "gpu_launches": args.steps * (1 + hm.num_groups),
     }
+    if lockfree:
+        line["lockfree"] = lockfree
     print(json.dumps(line), flush=True)
+
+
+def _lockfree(args, buf, hm, hyper, grads, P, device):
+    """C3's "lock-free delayed update" (Algorithm 2) on the
+    same pools: actors.LockFreeRunner with the host-tier sweep as the
+    updating actor and, as the GPU actor, the slice's forward+backward
+    modelled as a spin of 6 x params x tokens / (measured bf16 peak x MFU) —
+    the update path is the product here, not the model.  delay=0 is the
+    synchronous loop (update, then the next compute); delay=1 overlaps the
+    update of step k with the compute of step k+1 (staleness <= 1)."""
+    from pathlib import Path
+    from . import _device as Dv
+    from . import _native as Nn
+    from .actors import LockFreeRunner
+    peaks = Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    bf16 = json.loads(peaks.read_text()).get("bf16_tflops_sustained", 1369.5) if peaks.exists() else 1369.5
+    tokens, mfu = args.c3_tokens, 0.5
+    tc_ms = 6.0 * P * tokens / (bf16 * 1e12 * mfu) * 1e3
+    zero = torch.zeros((), device=device)
+
+    def grads_fn(params, it):
+        Dv.check(Nn.lib().hm_spin(int(tc_ms * 1e6), Dv.sptr(torch.cuda.current_stream(device))))
+        return zero, grads
+
+    out = {"gpu_actor": f"spin of 6 x {P} params x {tokens} tokens / ({bf16} TF/s x MFU {mfu})",
+           "compute_ms": tc_ms, "iters": args.c3_lockfree_iters}
+    for delay, name in ((0, "sync"), (1, "lockfree")):
+        runner = LockFreeRunner(buf, hm, hyper, delay=delay)
+        runner.run(1, grads_fn, mode=name)                     # warm-up iteration
+        rep = runner.run(args.c3_lockfree_iters, grads_fn, mode=name)
+        out[f"{name}_iter_ms"] = rep.iter_ms
+        out[f"{name}_max_staleness"] = rep.max_staleness
+    out["speedup"] = out["sync_iter_ms"] / out["lockfree_iter_ms"]
+    return out
