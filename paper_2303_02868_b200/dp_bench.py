@@ -101,7 +101,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     def do_step(**kw):
         if pipelined:
             return dp.step_pipelined(hyper, args.dp_groups, reduce_ctas=args.dp_reduce_ctas,
-                                     update_ctas=args.dp_update_ctas, **kw)
+                                     update_ctas=args.dp_update_ctas, reduce_sms=args.dp_reduce_sms, **kw)
         return dp.step(hyper, **kw)
     flat = owned_grad_flat(layout, args.dtype, device, 7 + rank)
     for rnd in range(2):  # fill both gradient page buffers (K3)
@@ -199,6 +199,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                    "dp_groups": args.dp_groups if pipelined else 1,
                    "dp_reduce_ctas": args.dp_reduce_ctas if pipelined else 0,
                    "dp_update_ctas": args.dp_update_ctas if pipelined else 0,
+                   "dp_reduce_sms": args.dp_reduce_sms if pipelined else 0,
                    "ag_publish": ["per-thread stores", "bulk", "bulk+wait"][args.ag_publish],
                    "step": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
                             "page-Adam(bucket) || AG(bucket)") if not fused else

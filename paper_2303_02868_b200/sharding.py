@@ -288,6 +288,27 @@ class FusedShardedPageStep:
         import ctypes as C
         return (C.c_uint64 * len(ptrs))(*ptrs)
 
+    def _green_streams(self, reduce_sms: int):
+        """Two CUDA green contexts (disjoint SM partitions): ``reduce_sms`` SMs
+        for the link-bound reduce, the rest for the HBM-bound update, so the
+        two kernels share the GPU by construction.  Streams wrapped as
+        torch.cuda streams; cached per partition size."""
+        cache = self.__dict__.setdefault("_green", {})
+        if reduce_sms not in cache:
+            G = torch.cuda.green_contexts
+            if not G.SUPPORTED:
+                raise ConfigError("this torch build has no CUDA green context support")
+            total = torch.cuda.get_device_properties(self.device).multi_processor_count
+            rest = (total - reduce_sms) // 8 * 8
+            if reduce_sms <= 0 or rest <= 0:
+                raise ConfigError(f"bad SM split {reduce_sms}/{total}")
+            g_rs = G.GreenContext.create(reduce_sms, self.device.index)
+            g_up = G.GreenContext.create(rest, self.device.index)
+            rs = torch.cuda.ExternalStream(g_rs.Stream().cuda_stream, device=self.device)
+            up = torch.cuda.ExternalStream(g_up.Stream().cuda_stream, device=self.device)
+            cache[reduce_sms] = (g_rs, g_up, rs, up)   # keep the contexts alive
+        return cache[reduce_sms][2], cache[reduce_sms][3]
+
     def _group_plan(self, groups: int):
         """Contiguous layer groups with their owned check / adam chunks."""
         cache = self.__dict__.setdefault("_gplans", {})
@@ -307,7 +328,7 @@ class FusedShardedPageStep:
         return cache[groups]
 
     def step_pipelined(self, hyper, groups: int = 4, *, reduce_ctas: int = 0, update_ctas: int = 0,
-                       ready=None, stream=None,
+                       reduce_sms: int = 0, ready=None, stream=None,
                        timings: dict | None = None):
         """``step`` with the layers cut into contiguous groups and two streams:
         the reduce-scatter + check of group k+1 runs while group k is updated
@@ -318,7 +339,9 @@ class FusedShardedPageStep:
         grid of that many CTAs on a high-priority stream: the link-bound
         reduce then runs from a few SMs beside the HBM-bound update of the
         previous group; ``update_ctas > 0`` likewise gives the update a
-        persistent grid of its own.  ``ready`` (one event per layer group,
+        persistent grid of its own; ``reduce_sms > 0`` instead runs the reduce
+        and the update in two CUDA green contexts (disjoint SM partitions).
+        ``ready`` (one event per layer group,
         from ``lockfree.ingest``) lets the step start while the gradient is
         still arriving from the host: group k is reduced once its own K3 has
         run on every rank.  With NVLS the RS leg is outbound-heavy (S out, S/N
@@ -334,6 +357,8 @@ class FusedShardedPageStep:
         if any(x != gsel for x in buf._gsel) or any(x != psel for x in buf._psel):
             raise ConfigError("DP page step expects all layers in the same page buffers")
         plan, rs, up = self._group_plan(groups)
+        if reduce_sms > 0:   # SM partitions instead of block-scheduler priority
+            rs, up = self._green_streams(reduce_sms)
         span_b = lay.elems16 * buf.g16_pool.element_size()
         span = lay.elems16
         lib, eng = N.lib(), ms._eng

@@ -85,7 +85,8 @@ def main():
             step.step_pipelined(hyper, groups, ready=ready)
         elif groups > 1 and mode != "nccl":
             step.step_pipelined(hyper, groups, reduce_ctas=int(os.environ.get("DP_REDUCE_CTAS", "0")),
-                                update_ctas=int(os.environ.get("DP_UPDATE_CTAS", "0")))
+                                update_ctas=int(os.environ.get("DP_UPDATE_CTAS", "0")),
+                                reduce_sms=int(os.environ.get("DP_REDUCE_SMS", "0")))
         else:
             step.step(hyper)
         # every owner's reduced (post reduce-scatter) pages, gathered so each

@@ -21,10 +21,13 @@ ROOT = Path(__file__).resolve().parent.parent
     (2, "bf16", "p2p", 3, 5),    # persistent reduce grid: 5 CTAs striding over the chunks
     (2, "bf16", "p2p", 1, "bulk1"), (2, "fp16", "p2p", 3, "bulk2"),    # bulk-copy AG epilogue
     (2, "bf16", "p2p", 3, "upd7"),    # persistent update grid (7 CTAs) + persistent reduce (5)
-    (2, "bf16", "p2p", 4, "ingest")])  # host gradient streamed in per group, step starts early
+    (2, "bf16", "p2p", 4, "ingest"),   # host gradient streamed in per group, step starts early
+    (2, "bf16", "p2p", 4, "green32")])  # reduce and update in two green contexts (SM partitions)
 def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
-    agp, upd, ingest = 0, 0, 0
-    if ctas == "ingest":
+    agp, upd, ingest, green = 0, 0, 0, 0
+    if isinstance(ctas, str) and ctas.startswith("green"):
+        green, ctas = int(ctas[5:]), 0
+    elif ctas == "ingest":
         ingest, ctas = 1, 0
     elif isinstance(ctas, str) and ctas.startswith("bulk"):
         agp, ctas = int(ctas[-1]), 0
@@ -36,7 +39,8 @@ def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
     world = 4 if n >= 4 else 2
     env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype, DP_MODE=mode, DP_GROUPS=str(groups),
                DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp),
-               DP_UPDATE_CTAS=str(upd), DP_INGEST=str(ingest))
+               DP_UPDATE_CTAS=str(upd), DP_INGEST=str(ingest),
+               DP_REDUCE_SMS=str(green))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29611", str(ROOT / "tests" / "dp_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
