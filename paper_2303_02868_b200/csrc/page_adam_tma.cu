@@ -71,16 +71,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// Every byte is touched once per sweep: both directions carry an L2
+// evict-first policy so the stream does not displace reusable lines (the
+// LDG kernel's .L2::evict_first on its 256-bit accesses, as a TMA hint).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_u32(src)), "r"(bytes)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+               ::"l"(dst), "r"(smem_u32(src)), "r"(bytes), "l"(pol)
                : "memory");
 }
 __device__ __forceinline__ void consumers_sync() {
@@ -129,6 +138,7 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ int vecflag[kMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol = evict_first_policy();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -153,10 +163,10 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
         if (vec) {
           const uint32_t gb = c.n * kGE, fb = c.n * 4;
           mbar_expect_tx(&full[s], gb + 3 * fb);
-          bulk_g2s(st, static_cast<const char*>(g) + go * kGE, gb, &full[s]);
-          bulk_g2s(st + L::kOffP, p32 + so, fb, &full[s]);
-          bulk_g2s(st + L::kOffM, m32 + so, fb, &full[s]);
-          bulk_g2s(st + L::kOffV, v32 + so, fb, &full[s]);
+          bulk_g2s(st, static_cast<const char*>(g) + go * kGE, gb, &full[s], pol);
+          bulk_g2s(st + L::kOffP, p32 + so, fb, &full[s], pol);
+          bulk_g2s(st + L::kOffM, m32 + so, fb, &full[s], pol);
+          bulk_g2s(st + L::kOffV, v32 + so, fb, &full[s], pol);
         } else {
           mbar_arrive(&full[s]);  // consumers take this chunk straight from global memory
         }
@@ -201,12 +211,12 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (r.apply) {
-          bulk_s2g(p32 + so, st + L::kOffP, n * 4);
-          bulk_s2g(m32 + so, st + L::kOffM, n * 4);
-          bulk_s2g(v32 + so, st + L::kOffV, n * 4);
+          bulk_s2g(p32 + so, st + L::kOffP, n * 4, pol);
+          bulk_s2g(m32 + so, st + L::kOffM, n * 4, pol);
+          bulk_s2g(v32 + so, st + L::kOffV, n * 4, pol);
         }
         if constexpr (kPub)
-          bulk_s2g(static_cast<typename Elem<PDT>::T*>(p16) + po, st + L::kOffP16, n * 2);
+          bulk_s2g(static_cast<typename Elem<PDT>::T*>(p16) + po, st + L::kOffP16, n * 2, pol);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         // Release the PREVIOUS stage once its stores have read shared memory
         // (at most this stage's group still reading): the store of chunk i
