@@ -29,7 +29,7 @@ namespace {
 constexpr int kMaxStages = 4;
 constexpr int kConsumerWarps = 16;  // the Adam chain is latency-bound per warp: 16 warps hide it
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kTmaThreads = kConsumers + 64;   // + producer warp + storer warp
+constexpr int kTmaThreads = kConsumers + 32;
 
 // One stage = one 4096-element chunk: g | p | m | v, and the 16-bit publish.
 // With a 16-bit gradient each thread writes its published granule over the
@@ -135,16 +135,13 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
   constexpr bool kPub = PDT != 0;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int kStages = L::kStages;
-  // full: loads landed (tx count); computed: consumers wrote the results;
-  // empty: the stores have read the stage, the producer may refill it.
-  __shared__ __align__(8) uint64_t full[kMaxStages], computed[kMaxStages], empty[kMaxStages];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ int vecflag[kMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t pol = evict_first_policy();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&computed[s], 1);
       mbar_init(&empty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -152,7 +149,7 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
   __syncthreads();
   const int iters = blockIdx.x < n_chunks ? (n_chunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (warp == kConsumerWarps) {  // ---- producer: bulk loads into free stages ----
+  if (warp == kConsumerWarps) {  // ---- producer ----
     if (lane == 0) {
       for (int it = 0; it < iters; ++it) {
         const int s = it % kStages;
@@ -178,36 +175,9 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
     return;
   }
 
-  if (warp == kConsumerWarps + 1) {  // ---- storer: bulk stores of computed stages ----
-    if (lane == 0) {
-      for (int it = 0; it < iters; ++it) {
-        const int s = it % kStages;
-        mbar_wait(&computed[s], (it / kStages) & 1);
-        if (vecflag[s]) {
-          const hm_adam_chunk c = chunks[blockIdx.x + it * gridDim.x];
-          const hm_group_launch gl = groups[c.slot];
-          const uint64_t so = c.s_off, po = c.p_off + gl.p_shift;
-          const uint32_t n = c.n;
-          unsigned char* st = smem + s * L::kBytes;
-          if (rt[c.slot].apply) {
-            bulk_s2g(p32 + so, st + L::kOffP, n * 4, pol);
-            bulk_s2g(m32 + so, st + L::kOffM, n * 4, pol);
-            bulk_s2g(v32 + so, st + L::kOffV, n * 4, pol);
-          }
-          if constexpr (kPub)
-            bulk_s2g(static_cast<typename Elem<PDT>::T*>(p16) + po, st + L::kOffP16, n * 2, pol);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // stage read out
-        }
-        mbar_arrive(&empty[s]);
-      }
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");            // writes performed
-    }
-    return;
-  }
-
-  // ---- consumers: the Adam chain on the staged chunk ----
+  // ---- consumers ----
   const int tid = threadIdx.x;
+  int pending = -1;  // stage whose bulk stores may still be reading shared memory (thread 0)
   for (int it = 0; it < iters; ++it) {
     const int s = it % kStages;
     mbar_wait(&full[s], (it / kStages) & 1);
@@ -237,9 +207,26 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
         }
         if constexpr (kPub) smem_store8h<PDT>(st + L::kOffP16, e, pv);
       }
-      // make this thread's shared-memory writes visible to the async proxy
-      // (the storer's bulk copies) before the hand-off
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      consumers_sync();  // the stage holds the results
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (r.apply) {
+          bulk_s2g(p32 + so, st + L::kOffP, n * 4, pol);
+          bulk_s2g(m32 + so, st + L::kOffM, n * 4, pol);
+          bulk_s2g(v32 + so, st + L::kOffV, n * 4, pol);
+        }
+        if constexpr (kPub)
+          bulk_s2g(static_cast<typename Elem<PDT>::T*>(p16) + po, st + L::kOffP16, n * 2, pol);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // Release the PREVIOUS stage once its stores have read shared memory
+        // (at most this stage's group still reading): the store of chunk i
+        // drains while chunk i+1 is computed.
+        if (pending >= 0) {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          mbar_arrive(&empty[pending]);
+        }
+        pending = s;
+      }
     } else {
       for (uint32_t i = tid; i < n; i += kConsumers) {
         float p = p32[so + i];
@@ -252,9 +239,23 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
         }
         if constexpr (kPub) store1<PDT>(p16, po + i, p);
       }
+      consumers_sync();
+      if (tid == 0) {
+        if (pending >= 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(&empty[pending]);
+          pending = -1;
+        }
+        mbar_arrive(&empty[s]);
+      }
     }
-    consumers_sync();                        // every consumer is done with stage s
-    if (tid == 0) mbar_arrive(&computed[s]);
+  }
+  if (tid == 0) {
+    if (pending >= 0) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mbar_arrive(&empty[pending]);
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 }
 
