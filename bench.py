@@ -138,12 +138,18 @@ class CpuReferenceSample:
         self.pool.shutdown()
 
 
-def cpu_reference_sample(specs, page_bytes, sample_pages: int, threads: int, dtype: str, reps: int):
+def cpu_reference_sample(specs, page_bytes, sample_pages: int, threads: int, dtype: str,
+                         min_seconds: float = 10.0, min_reps: int = 2):
+    """Passes over the bounded sample until ``min_seconds`` of CPU work (and
+    at least ``min_reps`` passes) have run; returns (params per pass, median
+    pass time, passes)."""
     s = CpuReferenceSample(page_bytes, sample_pages, threads, dtype)
     s.run()  # warm
-    best = min(s.run() for _ in range(reps))
+    times = []
+    while len(times) < min_reps or sum(times) < min_seconds:
+        times.append(s.run())
     s.close()
-    return s.n, best
+    return s.n, statistics.median(times), len(times)
 
 
 def run_reference(args):
@@ -291,11 +297,12 @@ def run_ours_single(args):
     Dv.restore_affinity(numa)   # the CPU baseline gets every host core
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        n, t = cpu_reference_sample(specs, page, args.cpu_sample_pages, threads, args.dtype, reps=2)
+        n, t, passes = cpu_reference_sample(specs, page, args.cpu_sample_pages, threads, args.dtype,
+                                            min_seconds=args.cpu_seconds)
         cpu = {"value": n / t, "unit": "params/s", "cores": threads, "kind": "port",
                "sample": f"first {args.cpu_sample_pages} pages ({n} params) of the {args.config} pool; "
                          "take->apply_update->publish restated op-for-op in numpy (oracle/page_adam.py), "
-                         f"{threads} threads, best of 2"}
+                         f"{threads} threads, median of {passes} passes (>= {args.cpu_seconds:g} s of CPU work)"}
     line = {
         "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -409,6 +416,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-groups", type=int, default=8)
     ap.add_argument("--cpu-sample-pages", type=int, default=32)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="GPU arm's cpu_baseline: repeat the sample for at least this much CPU work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c3-layers", type=int, default=8, help="C3 slice (host-memory bound)")
     ap.add_argument("--c3-lockfree-iters", type=int, default=4,

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 def test_bench_line_keys(cuda):
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "5",
-                          "--warmup", "3", "--e2e-steps", "1", "--cpu-sample-pages", "1"],
+                          "--warmup", "3", "--e2e-steps", "1", "--cpu-sample-pages", "1", "--cpu-seconds", "1"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
