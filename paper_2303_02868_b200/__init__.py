@@ -31,7 +31,12 @@ _LAZY = {
     "AdamHyper": "lockfree", "DelayModel": "lockfree", "GradMessage": "lockfree",
     "MasterState": "lockfree", "ParamBuffer": "lockfree", "ConservationLedger": "lockfree",
     "accumulate_gradient": "lockfree", "apply_update": "lockfree", "publish_params": "lockfree",
-    "sweep": "lockfree", "ingest_sweep": "lockfree", "ShardingModel": "sharding",
+    "sweep": "lockfree", "ingest_sweep": "lockfree", "ingest": "lockfree",
+    "ShardingModel": "sharding", "ShardedPageStep": "sharding",
+    "FusedShardedPageStep": "sharding", "symmetric_alloc": "sharding",
+    "HostMasterState": "swap", "swap_sweep": "swap", "SSDMasterState": "ssd", "ssd_sweep": "ssd",
+    "DevicePageManager": "pages", "LockFreeRunner": "actors", "ScheduleExecutor": "executor",
+    "PageLayout": "layout",
 }
 
 __version__ = "0.1.0"
