@@ -95,3 +95,13 @@ def test_ctypes_arity_matches_header():
         params = params.strip()
         n = 0 if params in ("", "void") else params.count(",") + 1
         assert n == len(N.SIGNATURES[name][1]), f"{name}: header {n} params, ctypes {len(N.SIGNATURES[name][1])}"
+
+
+def test_package_exports_resolve():
+    """Every name the package re-exports resolves (the reference's names for
+    the path plus the build's own entry points); importing needs no GPU."""
+    import paper_2303_02868_b200 as P
+    for name in P._LAZY:
+        assert getattr(P, name) is not None, name
+    for name in ("PageManager", "TierPool", "pool_init", "TensorSpec", "ConfigError"):
+        assert hasattr(P, name)
