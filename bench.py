@@ -303,6 +303,10 @@ def run_ours_single(args):
                "sample": f"first {args.cpu_sample_pages} pages ({n} params) of the {args.config} pool; "
                          "take->apply_update->publish restated op-for-op in numpy (oracle/page_adam.py), "
                          f"{threads} threads, median of {passes} passes (>= {args.cpu_seconds:g} s of CPU work)"}
+        # the reference itself is single-threaded numpy: one thread, for context
+        n1, t1, _ = cpu_reference_sample(specs, page, max(1, args.cpu_sample_pages // 8), 1, args.dtype,
+                                         min_seconds=min(2.0, args.cpu_seconds))
+        cpu["single_thread_value"] = n1 / t1
     line = {
         "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
