@@ -448,6 +448,15 @@ def main():
         from paper_2303_02868_b200 import swap_bench
         return swap_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # plain `python bench.py --gpus N`: relaunch as N ranks, one per GPU
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                   f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]])
     if world > 1 or args.gpus > 1:
         from paper_2303_02868_b200 import dp_bench
         return dp_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks, build_state)
