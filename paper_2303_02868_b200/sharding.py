@@ -404,39 +404,41 @@ class FusedShardedPageStep:
         rts = self.__dict__.setdefault("_rts", {})
         D.check(lib.hm_set_dp_reduce_ctas(int(reduce_ctas)))   # persistent reduce grid (0 = per chunk)
         D.check(lib.hm_set_dp_update_ctas(int(update_ctas)))   # persistent update grid (0 = per chunk)
-        for k, (grp, check, adam) in enumerate(plan):
-            first, n = grp[0], len(grp)
-            with torch.cuda.stream(rs):
-                if ready is not None:
-                    rs.wait_event(ready[k])
-                    self.h_g.barrier(channel=0)                  # group k landed on every rank
-                D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
-                                               D.ptr(eng.desc.static(check)), len(check),
-                                               D.ptr(self.flags_local), None, D.sptr(rs)))
-                self.h_f.barrier(channel=1)                      # group k's flags visible everywhere
-                done = torch.cuda.Event()
-                done.record(rs)
-            up.wait_event(done)
-            with torch.cuda.stream(up):
-                D.check(lib.hm_dp_flags_merge(self._arr([p + 4 * first for p in self.f_ptrs]), None,
-                                              self.n, n, D.ptr(self.flags) + 4 * first, None, D.sptr(up)))
-                rows = np.zeros(n, dtype=N.GROUP_LAUNCH)
-                for i, l in enumerate(grp):
-                    rows[i] = (gsel * span, (psel ^ 1) * span, l, l)
-                dgroups = eng.desc.table(rows)
-                if (k, n) not in rts:
-                    rts[(k, n)] = torch.empty(n * N.GROUP_RT_BYTES, dtype=torch.uint8, device=self.device)
-                rt = rts[(k, n)]
-                D.check(lib.hm_adam_prologue(D.ptr(dgroups), n, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
-                                             D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(self.flags),
-                                             None, 1, D.sptr(up)))
-                D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups),
-                                            D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
-                                            D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
-                                            self.n, self.mc_p if self.mc_p else None, buf._dt, hc,
-                                            D.sptr(up)))
-        D.check(lib.hm_set_dp_reduce_ctas(0))
-        D.check(lib.hm_set_dp_update_ctas(0))
+        try:
+            for k, (grp, check, adam) in enumerate(plan):
+                first, n = grp[0], len(grp)
+                with torch.cuda.stream(rs):
+                    if ready is not None:
+                        rs.wait_event(ready[k])
+                        self.h_g.barrier(channel=0)                  # group k landed on every rank
+                    D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
+                                                   D.ptr(eng.desc.static(check)), len(check),
+                                                   D.ptr(self.flags_local), None, D.sptr(rs)))
+                    self.h_f.barrier(channel=1)                      # group k's flags visible everywhere
+                    done = torch.cuda.Event()
+                    done.record(rs)
+                up.wait_event(done)
+                with torch.cuda.stream(up):
+                    D.check(lib.hm_dp_flags_merge(self._arr([p + 4 * first for p in self.f_ptrs]), None,
+                                                  self.n, n, D.ptr(self.flags) + 4 * first, None, D.sptr(up)))
+                    rows = np.zeros(n, dtype=N.GROUP_LAUNCH)
+                    for i, l in enumerate(grp):
+                        rows[i] = (gsel * span, (psel ^ 1) * span, l, l)
+                    dgroups = eng.desc.table(rows)
+                    if (k, n) not in rts:
+                        rts[(k, n)] = torch.empty(n * N.GROUP_RT_BYTES, dtype=torch.uint8, device=self.device)
+                    rt = rts[(k, n)]
+                    D.check(lib.hm_adam_prologue(D.ptr(dgroups), n, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
+                                                 D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(self.flags),
+                                                 None, 1, D.sptr(up)))
+                    D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups),
+                                                D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
+                                                D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
+                                                self.n, self.mc_p if self.mc_p else None, buf._dt, hc,
+                                                D.sptr(up)))
+        finally:   # process-wide knobs: never leak a persistent grid into later launches
+            D.check(lib.hm_set_dp_reduce_ctas(0))
+            D.check(lib.hm_set_dp_update_ctas(0))
         mark("rs", rs)
         st.wait_stream(rs)
         st.wait_stream(up)
