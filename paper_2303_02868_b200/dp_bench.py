@@ -95,7 +95,10 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     from . import _native as NL
     NL.check(NL.lib().hm_set_ag_publish(args.ag_publish))
     if args.dp_groups < 0:   # auto: measured policy (profiles/r1_dp_c2.md)
-        args.dp_groups, args.dp_reduce_ctas = (8, 128) if world == 2 else (1, 0)
+        # pipelining pays at N=2 once the per-group barriers are small next to
+        # the transfer (C2/C4/C5, >= 1 GB of 16-bit pages), not for C1 (0.25 GB)
+        big = 2 * P >= 1e9
+        args.dp_groups, args.dp_reduce_ctas = (8, 128) if world == 2 and big else (1, 0)
     pipelined = fused and args.dp_groups > 1
 
     def do_step(**kw):
