@@ -399,7 +399,8 @@ def main():
     ap.add_argument("--dp-groups", type=int, default=-1,
                     help="fused DP step: >1 pipelines the reduce-scatter of layer group k+1 with the "
                          "update + all-gather of group k; -1 = auto (8 groups with a 128-CTA reduce "
-                         "grid at N=2, where the update is HBM-bound; 1 at N>=4, where the whole "
+                         "grid at N=2 for >= 1 GB of 16-bit pages, where the update is HBM-bound; "
+                         "1 otherwise and at N>=4, where the whole "
                          "step is NVLink-bound — profiles/r1_dp_c2.md)")
     ap.add_argument("--ag-publish", type=int, default=0, choices=[0, 1, 2],
                     help="fused DP all-gather epilogue: 0 per-thread peer stores, 1 per-CTA bulk "
