@@ -216,6 +216,10 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
  * of one layer group can share the SMs with the page-Adam of the previous
  * group (layer-group pipelined DP step).  Process-wide. */
 int hm_set_dp_reduce_ctas(int ctas);
+/* Minimum peer-array width (0 = the peer count rounded up to 2/4/8) of the
+ * reduce kernel, so the 8-wide instantiation can be exercised on a 2- or
+ * 4-GPU box.  Same results at every width.  Process-wide. */
+int hm_set_dp_reduce_width(int width);
 /* flags_out[l] = OR_r peer_flags_r[l]; sumsq_out[l] = sum_r peer_sumsq_r[l]
  * (rank order).  Replaces an all-reduce of the per-layer reject flags. */
 int hm_dp_flags_merge(const uint64_t* peer_flags, const uint64_t* peer_sumsq, int n_peers,

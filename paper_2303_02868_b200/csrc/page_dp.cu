@@ -212,6 +212,7 @@ __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, in
 using RcFn = void (*)(const hm_seg_chunk*, int, PeerPtrs, const char*, void*, uint32_t*, double*);
 
 std::atomic<int> g_reduce_ctas{0};   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
+std::atomic<int> g_reduce_width{0};  // minimum peer-array width of the reduce kernel (test hook)
 
 // Chunks per pass of the persistent grid: as deep as the registers allow.
 template <int NP>
@@ -267,13 +268,24 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
   const int rctas = hm::g_reduce_ctas.load(std::memory_order_relaxed);
   const bool persistent = rctas > 0;
   int depth = 1;
-  hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, n_peers, persistent, &depth);
+  // template width: the peer count rounded up to 2/4/8, or wider if forced
+  // (hm_set_dp_reduce_width: runs the 8-wide kernel on a 2- or 4-GPU box)
+  const int width = n_peers > hm::g_reduce_width.load(std::memory_order_relaxed)
+                        ? n_peers : hm::g_reduce_width.load(std::memory_order_relaxed);
+  hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, width, persistent, &depth);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
   const int64_t passes = (n_chunks + depth - 1) / depth;
   const int64_t grid = persistent && rctas < passes ? rctas : passes;
   fn<<<(unsigned)grid, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, (int)n_chunks, peers, static_cast<const char*>(mc_pool), local_pool, nonfinite, sumsq);
   HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_set_dp_reduce_width(int width) {
+  if (width < 0 || width > hm::kMaxPeers)
+    return hm_set_error(HM_ERR_INVALID, "hm_set_dp_reduce_width: 0..%d, got %d", hm::kMaxPeers, width);
+  hm::g_reduce_width = width;
   return HM_OK;
 }
 
