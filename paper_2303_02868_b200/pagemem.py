@@ -308,7 +308,8 @@ class PageManager:
     (hiermem/pagemem.py:188-446)."""
 
     def __init__(self, pool_specs):
-        """pool_specs: iterable of (tier, capacity_bytes) or (tier, capacity_bytes, page_bytes)."""
+        """``pool_specs``: ``(tier, capacity)`` or ``(tier, capacity, page_bytes)`` entries;
+        page ids are handed out pool after pool in this order."""
         self._t = _Table()
         self.pools: dict[Tier, TierPool] = {}
         for entry in pool_specs:
@@ -330,16 +331,16 @@ class PageManager:
     def pool(self, tier) -> TierPool:
         tier = Tier.parse(tier)
         if tier not in self.pools:
-            raise ConfigError(f"no pool configured for tier {tier.name}")
+            raise ConfigError(f"this manager has no {tier.name} pool")
         return self.pools[tier]
 
     def page(self, page_id: int) -> Page:
         for pool in self.pools.values():
             if page_id in pool.pages:
                 return pool.pages[page_id]
-        raise KeyError(f"unknown page id {page_id}")
+        raise KeyError(f"page {page_id} belongs to no pool")
 
-    # -- allocation ---------------------------------------------------------
+    # allocate / release
 
     def allocate(self, spec, tier) -> ManagedTensor:
         pool = self.pool(tier)
@@ -353,13 +354,13 @@ class PageManager:
 
     def release(self, tensor_id: int) -> int:
         if tensor_id not in self.tensors:
-            raise KeyError(f"unknown or already released tensor {tensor_id}")
+            raise KeyError(f"tensor {tensor_id} is not live")
         freed = C.c_int64()
         self._t.call("hm_pt_release", C.c_int64(tensor_id), C.byref(freed))
         del self.tensors[tensor_id]
         return freed.value
 
-    # -- movement -----------------------------------------------------------
+    # page motion between tiers
 
     def page_move(self, page_id: int, target_tier) -> TransferDescriptor:
         target = Tier.parse(target_tier)
@@ -367,19 +368,20 @@ class PageManager:
         self._t.call("hm_pt_page_move", C.c_int64(page_id), int(target.value), out)
         return TransferDescriptor(out[0], Tier(out[1]), Tier(out[2]), out[3], out[4])
 
-    # -- defragmentation ----------------------------------------------------
+    # merge
 
     def tensor_merge(self, tensor_id: int) -> dict:
-        """Reassign a tensor's pages to a consecutive page-id run in its tier."""
+        """Defragment: move the tensor onto consecutive page ids of its tier
+        (the native table picks the run; the reference's rules and report)."""
         if tensor_id not in self.tensors:
-            raise KeyError(f"unknown tensor {tensor_id}")
+            raise KeyError(f"tensor {tensor_id} is not live")
         out = (C.c_int64 * 2)()
         self._t.call("hm_pt_tensor_merge", C.c_int64(tensor_id), out)
         n = len(self.tensors[tensor_id].page_list)
         return {"tensor_id": tensor_id, "contiguous": True,
                 "page_ids": list(range(out[1], out[1] + n)), "moved_chunks": out[0]}
 
-    # -- introspection ------------------------------------------------------
+    # state dump (the parity artefact)
 
     def state_dict(self) -> dict:
         pools = {}
@@ -429,10 +431,10 @@ def _manager_of(pool: TierPool) -> PageManager:
 
 
 def tensor_allocate(pool: TierPool, spec) -> ManagedTensor:
-    """Allocate a tensor into a standalone pool under the packing policy."""
+    """``PageManager.allocate`` on a pool used on its own (one implicit manager per pool)."""
     return _manager_of(pool).allocate(spec, pool.tier)
 
 
 def tensor_release(pool: TierPool, tensor_id: int) -> int:
-    """Release a tensor from a standalone pool; returns freed occupant bytes."""
+    """``PageManager.release`` on a pool used on its own; the occupant bytes freed."""
     return _manager_of(pool).release(tensor_id)
