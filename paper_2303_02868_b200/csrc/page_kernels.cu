@@ -82,25 +82,40 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
         if (e < c.n) ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
       }
     }
+    if (add) {
 #pragma unroll
-    for (int k = 0; k < kSegVecPer; ++k) {
-      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-      if (e >= c.n) continue;
-      F8 a, b, o;
-      decode<SDT>(ra[k], a);
-      if (add) decode<DDT>(rb[k], b);
-      else {
+      for (int k = 0; k < kSegVecPer; ++k) {
+        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
+        if (e >= c.n) continue;
+        F8 a, b, o;
+        decode<SDT>(ra[k], a);
+        decode<DDT>(rb[k], b);
 #pragma unroll
-        for (int j = 0; j < kVec; ++j) b.v[j] = 0.0f;
+        for (int j = 0; j < kVec; ++j) {
+          const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b.v[j], a.v[j])));
+          bad |= !is_finite(r);
+          if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b.v[j], b.v[j]));
+          o.v[j] = r;
+        }
+        store8<DDT>(dst, c.dst_off + e, o);
       }
+    } else {   // first message after a take: the buffer holds zeros, r = 0 + a
 #pragma unroll
-      for (int j = 0; j < kVec; ++j) {
-        const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b.v[j], a.v[j])));
-        bad |= !is_finite(r);
-        if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b.v[j], b.v[j]));
-        o.v[j] = r;
+      for (int k = 0; k < kSegVecPer; ++k) {
+        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
+        if (e >= c.n) continue;
+        F8 a, o;
+        decode<SDT>(ra[k], a);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) {
+          // 0 + a keeps the reference's -0 -> +0; r*r - 0*0 == r*r exactly
+          const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(0.0f, a.v[j])));
+          bad |= !is_finite(r);
+          if (sumsq) sq += __fmul_rn(r, r);
+          o.v[j] = r;
+        }
+        store8<DDT>(dst, c.dst_off + e, o);
       }
-      store8<DDT>(dst, c.dst_off + e, o);
     }
   } else {
     for (uint32_t i = tid; i < c.n; i += kSegThreads) {
