@@ -220,6 +220,9 @@ int hm_set_dp_reduce_ctas(int ctas);
  * reduce kernel, so the 8-wide instantiation can be exercised on a 2- or
  * 4-GPU box.  Same results at every width.  Process-wide. */
 int hm_set_dp_reduce_width(int width);
+/* 1: hm_dp_reduce_check pulls 32 B per thread and peer (256-bit loads, 16
+ * elements) instead of 16 B; same bits.  0 (default).  Process-wide. */
+int hm_set_dp_reduce_wide(int wide);
 /* flags_out[l] = OR_r peer_flags_r[l]; sumsq_out[l] = sum_r peer_sumsq_r[l]
  * (rank order).  Replaces an all-reduce of the per-layer reject flags. */
 int hm_dp_flags_merge(const uint64_t* peer_flags, const uint64_t* peer_sumsq, int n_peers,

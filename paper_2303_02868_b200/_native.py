@@ -77,6 +77,7 @@ SIGNATURES = {
     "hm_set_adam_variant": (_INT, [_INT]),
     "hm_set_dp_reduce_ctas": (_INT, [_INT]),
     "hm_set_dp_reduce_width": (_INT, [_INT]),
+    "hm_set_dp_reduce_wide": (_INT, [_INT]),
     "hm_set_ag_publish": (_INT, [_INT]),
     "hm_set_dp_update_ctas": (_INT, [_INT]),
     "hm_adam_prologue": (_INT, [_P, _I32, _P, C.POINTER(AdamHyperC), _P, _I64, _I64, _P, _P, _P,

@@ -195,6 +195,62 @@ reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, int n_chunks, PeerP
     reduce_chunks<DT, MC, NP, M>(chunks, i, n_chunks, peers, mc, local, nonfinite, sumsq);
 }
 
+// 256-bit peer loads: each thread pulls 16 contiguous elements (32 B) from
+// every peer in one access instead of two 16 B ones (hm_set_dp_reduce_wide).
+// Same rank-order f32 sum, so the same bits; chunks not 32 B aligned fall
+// back to the 16 B path.
+__device__ __forceinline__ void ld_peer_u8(const void* p, uint32_t (&u)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),
+                 "=r"(u[6]), "=r"(u[7])
+               : "l"(p));
+}
+
+template <int DT, int NP>
+__global__ void __launch_bounds__(kThreads)
+reduce_check_wide_kernel(const hm_seg_chunk* __restrict__ chunks, int n_chunks, PeerPtrs peers,
+                         const char* mc, void* __restrict__ local, uint32_t* __restrict__ nonfinite,
+                         double* __restrict__ sumsq) {
+  using T = typename Elem<DT>::T;
+  static_assert(kChunk == kThreads * 16, "16 elements per thread");
+  const hm_seg_chunk c = chunks[blockIdx.x];
+  const uint64_t off = c.src_off;
+  if (((off | (uint64_t)c.n) & 15) != 0) {
+    reduce_chunks<DT, false, NP, 1>(chunks, blockIdx.x, n_chunks, peers, mc, local, nonfinite, sumsq);
+    return;
+  }
+  const uint32_t e = (uint32_t)threadIdx.x * 16;
+  bool bad = false;
+  float sq = 0.f;
+  if (e < c.n) {
+    uint32_t u[NP][8];
+#pragma unroll
+    for (int r = 0; r < NP; ++r)
+      if (r < peers.n) ld_peer_u8(reinterpret_cast<const T*>(peers.p[r]) + off + e, u[r]);
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+#pragma unroll
+    for (int r = 0; r < NP; ++r) {
+      if (r >= peers.n) break;
+      const T* h = reinterpret_cast<const T*>(u[r]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = __fadd_rn(acc[j], Elem<DT>::widen(h[j]));
+    }
+    F8 o0, o1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float x = Elem<DT>::widen(Elem<DT>::narrow(acc[j]));
+      bad |= !is_finite(x);
+      sq += __fmul_rn(x, x);
+      if (j < 8) o0.v[j] = x; else o1.v[j - 8] = x;
+    }
+    store8<DT>(local, off + e, o0);
+    store8<DT>(local, off + e + 8, o1);
+  }
+  flush(bad, sq, nonfinite, sumsq, c.slot);
+}
+
 __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, int n,
                                    uint32_t* __restrict__ flags_out, double* __restrict__ sumsq_out) {
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
@@ -213,6 +269,17 @@ using RcFn = void (*)(const hm_seg_chunk*, int, PeerPtrs, const char*, void*, ui
 
 std::atomic<int> g_reduce_ctas{0};   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
 std::atomic<int> g_reduce_width{0};  // minimum peer-array width of the reduce kernel (test hook)
+std::atomic<int> g_reduce_wide{0};   // 1: 256-bit peer loads (hm_set_dp_reduce_wide)
+
+RcFn pick_rc_wide(int dt, int n) {
+  if (dt == HM_DT_BF16)
+    return n <= 2 ? reduce_check_wide_kernel<HM_DT_BF16, 2>
+                  : n <= 4 ? reduce_check_wide_kernel<HM_DT_BF16, 4> : reduce_check_wide_kernel<HM_DT_BF16, 8>;
+  if (dt == HM_DT_F16)
+    return n <= 2 ? reduce_check_wide_kernel<HM_DT_F16, 2>
+                  : n <= 4 ? reduce_check_wide_kernel<HM_DT_F16, 4> : reduce_check_wide_kernel<HM_DT_F16, 8>;
+  return nullptr;
+}
 
 // Chunks per pass of the persistent grid: as deep as the registers allow.
 template <int NP>
@@ -273,6 +340,8 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
   const int width = n_peers > hm::g_reduce_width.load(std::memory_order_relaxed)
                         ? n_peers : hm::g_reduce_width.load(std::memory_order_relaxed);
   hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, width, persistent, &depth);
+  if (fn && !persistent && mc_pool == nullptr && hm::g_reduce_wide.load(std::memory_order_relaxed))
+    fn = hm::pick_rc_wide(dtype, width);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
   const int64_t passes = (n_chunks + depth - 1) / depth;
   const int64_t grid = persistent && rctas < passes ? rctas : passes;
@@ -286,6 +355,11 @@ int hm_set_dp_reduce_width(int width) {
   if (width < 0 || width > hm::kMaxPeers)
     return hm_set_error(HM_ERR_INVALID, "hm_set_dp_reduce_width: 0..%d, got %d", hm::kMaxPeers, width);
   hm::g_reduce_width = width;
+  return HM_OK;
+}
+
+int hm_set_dp_reduce_wide(int wide) {
+  hm::g_reduce_wide = wide ? 1 : 0;
   return HM_OK;
 }
 

@@ -94,6 +94,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
     from . import _native as NL
     NL.check(NL.lib().hm_set_ag_publish(args.ag_publish))
+    NL.check(NL.lib().hm_set_dp_reduce_wide(args.dp_reduce_wide))
     if args.dp_groups < 0:   # auto: measured policy (profiles/r1_dp_c2.md)
         # pipelining pays at N=2 once the per-group barriers are small next to
         # the transfer (C2/C4/C5, >= 1 GB of 16-bit pages), not for C1 (0.25 GB)

@@ -132,6 +132,11 @@ def main():
         up_ms.append(phase(upd))
     lay = ranks[0]["lay"]
     S = 2 * sum(lay.numels)   # algorithmic bytes: the padding of the pool never moves
+    # reduce with 256-bit peer loads
+    D.check(lib.hm_set_dp_reduce_wide(1))
+    phase(rs)
+    rs_wide_ms = float(np.median([phase(rs) for _ in range(max(3, args.reps))]))
+    D.check(lib.hm_set_dp_reduce_wide(0))
     # update + AG with the bulk-copy publish epilogues
     upd_by_publish = {}
     for mode in args.ag_publish:
@@ -186,7 +191,7 @@ def main():
         "adam_ag_ms": t_up, "ag_busbw_gbs": bus(t_up), "ag_frac_770": bus(t_up) / 770.0,
         "adam_hbm_gbs": 28 * owned / (t_up / 1e3) / 1e9,
         "ce_pull_ms": ce_ms, "ce_pull_busbw_gbs": bus(ce_ms),
-        "reduce_ms_by_persistent_ctas": rs_by_ctas, "adam_ag_ms_by_publish_mode": upd_by_publish,
+        "reduce_ms_by_persistent_ctas": rs_by_ctas, "reduce_256bit_ms": rs_wide_ms, "adam_ag_ms_by_publish_mode": upd_by_publish,
         "rs_nvlink_bytes_in_per_gpu": S * (n - 1) / n, "ag_nvlink_bytes_out_per_gpu": S * (n - 1) / n,
     }))
 
