@@ -405,8 +405,8 @@ def main():
     ap.add_argument("--ag-publish", type=int, default=0, choices=[0, 1, 2],
                     help="fused DP all-gather epilogue: 0 per-thread peer stores, 1 per-CTA bulk "
                          "copies (cp.async.bulk), 2 bulk + wait for remote completion")
-    ap.add_argument("--dp-reduce-wide", type=int, default=0, choices=[0, 1],
-                    help="fused DP reduce with 256-bit peer loads (hm_set_dp_reduce_wide)")
+    ap.add_argument("--dp-reduce-wide", type=int, default=1, choices=[0, 1],
+                    help="fused DP reduce with 256-bit peer loads (hm_set_dp_reduce_wide; 0 = 16 B loads)")
     ap.add_argument("--dp-reduce-sms", type=int, default=0,
                     help="pipelined DP step: run the reduce and the update in two CUDA green "
                          "contexts, this many SMs for the reduce (0 = shared SMs)")

@@ -220,8 +220,10 @@ int hm_set_dp_reduce_ctas(int ctas);
  * reduce kernel, so the 8-wide instantiation can be exercised on a 2- or
  * 4-GPU box.  Same results at every width.  Process-wide. */
 int hm_set_dp_reduce_width(int width);
-/* 1: hm_dp_reduce_check pulls 32 B per thread and peer (256-bit loads, 16
- * elements) instead of 16 B; same bits.  0 (default).  Process-wide. */
+/* 1 (default): hm_dp_reduce_check pulls 32 B per thread and peer (256-bit
+ * loads, 16 elements; fewer read requests on the reverse link direction);
+ * 0: 16 B loads.  Same bits either way (the persistent grid always uses the
+ * 16 B form).  Process-wide. */
 int hm_set_dp_reduce_wide(int wide);
 /* flags_out[l] = OR_r peer_flags_r[l]; sumsq_out[l] = sum_r peer_sumsq_r[l]
  * (rank order).  Replaces an all-reduce of the per-layer reject flags. */

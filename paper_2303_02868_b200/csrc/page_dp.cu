@@ -196,9 +196,12 @@ reduce_check_kernel(const hm_seg_chunk* __restrict__ chunks, int n_chunks, PeerP
 }
 
 // 256-bit peer loads: each thread pulls 16 contiguous elements (32 B) from
-// every peer in one access instead of two 16 B ones (hm_set_dp_reduce_wide).
-// Same rank-order f32 sum, so the same bits; chunks not 32 B aligned fall
-// back to the 16 B path.
+// every peer in one access instead of two 16 B ones (hm_set_dp_reduce_wide,
+// on by default).  Same rank-order f32 sum, so the same bits; chunks not
+// 32 B aligned fall back to the 16 B path.  The payload on the link is the
+// same, but the read requests going the other way shrink by a quarter (ncu:
+// 494 -> 370 MB per GPU for C2 at N=4), and in the full step both directions
+// are busy: the reduce gets 4-5% faster (profiles/r1_nvlink_ncu.md).
 __device__ __forceinline__ void ld_peer_u8(const void* p, uint32_t (&u)[8]) {
   asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),
@@ -269,7 +272,7 @@ using RcFn = void (*)(const hm_seg_chunk*, int, PeerPtrs, const char*, void*, ui
 
 std::atomic<int> g_reduce_ctas{0};   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
 std::atomic<int> g_reduce_width{0};  // minimum peer-array width of the reduce kernel (test hook)
-std::atomic<int> g_reduce_wide{0};   // 1: 256-bit peer loads (hm_set_dp_reduce_wide)
+std::atomic<int> g_reduce_wide{1};   // 1: 256-bit peer loads (hm_set_dp_reduce_wide), the default
 
 RcFn pick_rc_wide(int dt, int n) {
   if (dt == HM_DT_BF16)

@@ -45,7 +45,8 @@ def main():
     from paper_2303_02868_b200 import _native as NL
     NL.check(NL.lib().hm_set_ag_publish(int(os.environ.get("DP_AG_PUBLISH", "0"))))
     NL.check(NL.lib().hm_set_dp_reduce_width(int(os.environ.get("DP_REDUCE_WIDTH", "0"))))
-    NL.check(NL.lib().hm_set_dp_reduce_wide(int(os.environ.get("DP_REDUCE_WIDE", "0"))))
+    if "DP_REDUCE_WIDE" in os.environ:
+        NL.check(NL.lib().hm_set_dp_reduce_wide(int(os.environ["DP_REDUCE_WIDE"])))
     if mode == "nvls" and step is None:
         sys.exit(0)
     from paper_2303_02868_b200.sharding import PageCollectives

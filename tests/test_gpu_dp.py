@@ -24,10 +24,10 @@ ROOT = Path(__file__).resolve().parent.parent
     (2, "bf16", "p2p", 4, "ingest"),   # host gradient streamed in per group, step starts early
     (2, "bf16", "p2p", 4, "green32"),  # reduce and update in two green contexts (SM partitions)
     (2, "bf16", "p2p", 1, "wide8"), (2, "fp16", "p2p", 3, "wide8"),  # 8-peer reduce kernel
-    (2, "bf16", "p2p", 1, "ld256")])   # 256-bit peer loads in the reduce
+    (2, "bf16", "p2p", 1, "ld128")])   # the 16 B-load reduce (256-bit loads are the default)
 def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
     agp, upd, ingest, green, width, ld256 = 0, 0, 0, 0, 0, 0
-    if ctas == "ld256":
+    if ctas == "ld128":
         ld256, ctas = 1, 0
     elif ctas == "wide8":   # the 8-wide reduce instantiation (what N=8 runs), with a persistent grid when pipelined
         width, ctas = 8, 5
@@ -46,8 +46,9 @@ def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
     env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype, DP_MODE=mode, DP_GROUPS=str(groups),
                DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp),
                DP_UPDATE_CTAS=str(upd), DP_INGEST=str(ingest),
-               DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width),
-               DP_REDUCE_WIDE=str(ld256))
+               DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width))
+    if ld256:
+        env["DP_REDUCE_WIDE"] = "0"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29611", str(ROOT / "tests" / "dp_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
