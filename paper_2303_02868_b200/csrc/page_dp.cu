@@ -209,76 +209,49 @@ __device__ __forceinline__ void ld_peer_u8(const void* p, uint32_t (&u)[8]) {
                : "l"(p));
 }
 
-template <int DT, int NP, int M>
-__device__ __forceinline__ void reduce_wide_chunks(const hm_seg_chunk* __restrict__ chunks, int first,
-                                                   int n_chunks, const PeerPtrs& peers, const char* mc,
-                                                   void* __restrict__ local,
-                                                   uint32_t* __restrict__ nonfinite,
-                                                   double* __restrict__ sumsq) {
-  using T = typename Elem<DT>::T;
-  static_assert(kChunk == kThreads * 16, "16 elements per thread");
-  const uint32_t e = (uint32_t)threadIdx.x * 16;
-  hm_seg_chunk c[M];
-  bool wide[M];
-  uint32_t u[M][NP][8];
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    if (first + m < n_chunks) {
-      c[m] = chunks[first + m];
-    } else {
-      c[m].src_off = 0;
-      c[m].n = 0;
-      c[m].slot = 0;
-    }
-    wide[m] = c[m].n > 0 && ((c[m].src_off | (uint64_t)c[m].n) & 15) == 0;
-    if (wide[m] && e < c[m].n) {
-#pragma unroll
-      for (int r = 0; r < NP; ++r)
-        if (r < peers.n) ld_peer_u8(reinterpret_cast<const T*>(peers.p[r]) + c[m].src_off + e, u[m][r]);
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    if (c[m].n == 0) continue;                 // uniform over the CTA
-    if (!wide[m]) {                            // not 32 B aligned: the 16 B path
-      reduce_chunks<DT, false, NP, 1>(chunks, first + m, n_chunks, peers, mc, local, nonfinite, sumsq);
-      continue;
-    }
-    bool bad = false;
-    float sq = 0.f;
-    if (e < c[m].n) {
-      float acc[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-#pragma unroll
-      for (int r = 0; r < NP; ++r) {
-        if (r >= peers.n) break;
-        const T* h = reinterpret_cast<const T*>(u[m][r]);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = __fadd_rn(acc[j], Elem<DT>::widen(h[j]));
-      }
-      F8 o0, o1;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float x = Elem<DT>::widen(Elem<DT>::narrow(acc[j]));
-        bad |= !is_finite(x);
-        sq += __fmul_rn(x, x);
-        if (j < 8) o0.v[j] = x; else o1.v[j - 8] = x;
-      }
-      store8<DT>(local, c[m].src_off + e, o0);
-      store8<DT>(local, c[m].src_off + e + 8, o1);
-    }
-    flush(bad, sq, nonfinite, sumsq, c[m].slot);
-  }
-}
-
-template <int DT, int NP, int M>
+template <int DT, int NP>
 __global__ void __launch_bounds__(kThreads)
 reduce_check_wide_kernel(const hm_seg_chunk* __restrict__ chunks, int n_chunks, PeerPtrs peers,
                          const char* mc, void* __restrict__ local, uint32_t* __restrict__ nonfinite,
                          double* __restrict__ sumsq) {
-  for (int i = blockIdx.x * M; i < n_chunks; i += gridDim.x * M)
-    reduce_wide_chunks<DT, NP, M>(chunks, i, n_chunks, peers, mc, local, nonfinite, sumsq);
+  using T = typename Elem<DT>::T;
+  static_assert(kChunk == kThreads * 16, "16 elements per thread");
+  const hm_seg_chunk c = chunks[blockIdx.x];
+  const uint64_t off = c.src_off;
+  if (((off | (uint64_t)c.n) & 15) != 0) {
+    reduce_chunks<DT, false, NP, 1>(chunks, blockIdx.x, n_chunks, peers, mc, local, nonfinite, sumsq);
+    return;
+  }
+  const uint32_t e = (uint32_t)threadIdx.x * 16;
+  bool bad = false;
+  float sq = 0.f;
+  if (e < c.n) {
+    uint32_t u[NP][8];
+#pragma unroll
+    for (int r = 0; r < NP; ++r)
+      if (r < peers.n) ld_peer_u8(reinterpret_cast<const T*>(peers.p[r]) + off + e, u[r]);
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+#pragma unroll
+    for (int r = 0; r < NP; ++r) {
+      if (r >= peers.n) break;
+      const T* h = reinterpret_cast<const T*>(u[r]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = __fadd_rn(acc[j], Elem<DT>::widen(h[j]));
+    }
+    F8 o0, o1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float x = Elem<DT>::widen(Elem<DT>::narrow(acc[j]));
+      bad |= !is_finite(x);
+      sq += __fmul_rn(x, x);
+      if (j < 8) o0.v[j] = x; else o1.v[j - 8] = x;
+    }
+    store8<DT>(local, off + e, o0);
+    store8<DT>(local, off + e + 8, o1);
+  }
+  flush(bad, sq, nonfinite, sumsq, c.slot);
 }
 
 __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, int n,
@@ -301,19 +274,13 @@ std::atomic<int> g_reduce_ctas{0};   // 0: one CTA per chunk; >0: persistent gri
 std::atomic<int> g_reduce_width{0};  // minimum peer-array width of the reduce kernel (test hook)
 std::atomic<int> g_reduce_wide{1};   // 1: 256-bit peer loads (hm_set_dp_reduce_wide), the default
 
-template <int DT>
-RcFn pick_rc_wide_dt(int n, bool persistent) {
-  // persistent grid: as many chunks in flight per CTA as the 16 B form keeps
-  // (M = 4/2/1 chunks of 16 B pairs = 2/1/1 chunks of 32 B accesses)
-  if (n <= 2) return persistent ? reduce_check_wide_kernel<DT, 2, 2> : reduce_check_wide_kernel<DT, 2, 1>;
-  if (n <= 4) return reduce_check_wide_kernel<DT, 4, 1>;
-  return reduce_check_wide_kernel<DT, 8, 1>;
-}
-
-RcFn pick_rc_wide(int dt, int n, bool persistent, int* depth) {
-  *depth = persistent && n <= 2 ? 2 : 1;
-  if (dt == HM_DT_BF16) return pick_rc_wide_dt<HM_DT_BF16>(n, persistent);
-  if (dt == HM_DT_F16) return pick_rc_wide_dt<HM_DT_F16>(n, persistent);
+RcFn pick_rc_wide(int dt, int n) {
+  if (dt == HM_DT_BF16)
+    return n <= 2 ? reduce_check_wide_kernel<HM_DT_BF16, 2>
+                  : n <= 4 ? reduce_check_wide_kernel<HM_DT_BF16, 4> : reduce_check_wide_kernel<HM_DT_BF16, 8>;
+  if (dt == HM_DT_F16)
+    return n <= 2 ? reduce_check_wide_kernel<HM_DT_F16, 2>
+                  : n <= 4 ? reduce_check_wide_kernel<HM_DT_F16, 4> : reduce_check_wide_kernel<HM_DT_F16, 8>;
   return nullptr;
 }
 
@@ -376,8 +343,8 @@ int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_p
   const int width = n_peers > hm::g_reduce_width.load(std::memory_order_relaxed)
                         ? n_peers : hm::g_reduce_width.load(std::memory_order_relaxed);
   hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, width, persistent, &depth);
-  if (fn && mc_pool == nullptr && hm::g_reduce_wide.load(std::memory_order_relaxed))
-    fn = hm::pick_rc_wide(dtype, width, persistent, &depth);
+  if (fn && !persistent && mc_pool == nullptr && hm::g_reduce_wide.load(std::memory_order_relaxed))
+    fn = hm::pick_rc_wide(dtype, width);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
   const int64_t passes = (n_chunks + depth - 1) / depth;
   const int64_t grid = persistent && rctas < passes ? rctas : passes;
