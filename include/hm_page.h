@@ -58,7 +58,7 @@ extern "C" {
 
 const char* hm_last_error(void);
 void        hm_last_error_bytes(int64_t* requested_bytes, int64_t* available_bytes);
-int         hm_abi_version(void);   /* bumped on any layout change below */
+int         hm_abi_version(void);   /* bumped on any layout change below (2) */
 int         hm_device_chunk_elems(void);  /* HM_ADAM_CHUNK, the kernel unit */
 
 /* ======================================================================== *
@@ -148,6 +148,20 @@ typedef struct hm_adam_hyper {
   float max_norm;     /* global grad-norm clip; <= 0 disables               */
 } hm_adam_hyper;
 
+/* Per-launch tuning (nullable; any field < 0 = the process default set by
+ * the matching hm_set_* call).  Launch settings travel with the launch, so
+ * two threads or streams with different settings never see each other's.
+ *   adam_threads  256 | 512 threads per 4096-element chunk (page-Adam)
+ *   adam_variant  0 LDG/STG streaming | 1 TMA bulk-copy pipeline
+ *   grid_ctas     hm_adam_main_ag / hm_dp_reduce_check: persistent grid size
+ *                 (0 = one CTA per chunk)
+ *   ag_publish    0 per-thread peer stores | 1 (or 2) staged bulk copies
+ *   reduce_width  minimum peer-array width of the reduce kernel (0, 2, 4, 8)
+ *   reduce_wide   1 = 256-bit peer loads | 0 = 128-bit                      */
+typedef struct hm_launch_opts {
+  int32_t adam_threads, adam_variant, grid_ctas, ag_publish, reduce_width, reduce_wide;
+} hm_launch_opts;
+
 /* Fused take -> update -> publish over page segments: one HBM pass reading
  * g (16-bit or f32) + p32/m32/v32 and writing p32/m32/v32 + p16.
  *   hiermem/lockfree.py:127-142 (apply_update), :155-165 (update_layer with
@@ -155,14 +169,19 @@ typedef struct hm_adam_hyper {
  * The prologue consumes nonfinite[flag] (computed when the gradient was
  * produced: hm_accumulate / hm_reduce_stats), advances steps[group] only
  * for applied groups, writes applied[group], clears the consumed flag and
- * sumsq when consume_flags != 0, and looks up bc1/bc2 in bc_table
+ * sumsq (and the ledger sum lsum[flag]) when consume_flags != 0, and
+ * looks up bc1/bc2 in bc_table
  * (pairs, index = step; must cover every reachable step).
  * explicit_step > 0 selects the functional apply_update form: the step is
  * given, steps[] is neither read nor written, and bc_table[0] holds its
  * (bc1, bc2).  p16 == NULL skips the publish cast.
  * On a rejected group nothing is written to p32/m32/v32; if p16 != NULL
  * the unchanged p32 is still cast (the reference publishes after a reject,
- * hiermem/lockfree.py:631-638). */
+ * hiermem/lockfree.py:631-638).
+ * Ledger (nullable): ledger_out[2i] = lsum[flag of group i] (the taken
+ * gradient's f64 sum, ConservationLedger.record_take, lockfree.py:237) and
+ * ledger_out[2i+1] = 1.0 if group i was applied else 0.0 (record_apply,
+ * lockfree.py:300), read before the consume resets lsum. */
 int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                  const hm_group_launch* groups, int32_t n_groups,
                  hm_group_rt* rt_scratch,
@@ -173,15 +192,15 @@ int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                  const float* bc_table, int64_t bc_len, int64_t explicit_step,
                  int32_t* steps, uint32_t* applied,
                  uint32_t* nonfinite, double* sumsq, int consume_flags,
+                 double* lsum, double* ledger_out, const hm_launch_opts* opts,
                  void* stream);
 
-/* Tuning knob of the page-Adam main kernel: 256 (default) or 512 threads per
- * 4096-element chunk (2 or 1 granule of 8 elements per thread).  Process-wide. */
+/* Process-wide DEFAULT of the page-Adam main kernel's threads per chunk: 256
+ * (default) or 512 (2 or 1 granule of 8 elements per thread). */
 int hm_set_adam_threads(int threads);
-/* Data-movement variant of the page-Adam main pass (same arithmetic, bytes and
- * results): 0 = LDG/STG streaming kernel (default), 1 = persistent TMA
- * bulk-copy pipeline (cp.async.bulk + mbarrier, 3 shared-memory stages per SM).
- * Process-wide. */
+/* Process-wide DEFAULT data-movement variant of the page-Adam main pass (same
+ * arithmetic, bytes and results): 0 = LDG/STG streaming kernel (default),
+ * 1 = persistent TMA bulk-copy pipeline (cp.async.bulk + mbarrier). */
 int hm_set_adam_variant(int variant);
 
 /* The two halves of hm_adam_step, for callers that pipeline the main pass
@@ -190,11 +209,12 @@ int hm_set_adam_variant(int variant);
 int hm_adam_prologue(const hm_group_launch* groups, int32_t n_groups, hm_group_rt* rt_scratch,
                      const hm_adam_hyper* hyper, const float* bc_table, int64_t bc_len,
                      int64_t explicit_step, int32_t* steps, uint32_t* applied,
-                     uint32_t* nonfinite, double* sumsq, int consume_flags, void* stream);
+                     uint32_t* nonfinite, double* sumsq, int consume_flags,
+                     double* lsum, double* ledger_out, void* stream);
 int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* groups,
                  const hm_group_rt* rt, const void* g, int g_dtype,
                  float* p32, float* m32, float* v32, void* p16, int p16_dtype,
-                 const hm_adam_hyper* hyper, void* stream);
+                 const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream);
 
 /* ---- data-parallel page collectives fused with compute (NVLink/NVSwitch) ---
  * Pools are symmetric buffers mapped into every rank (peer virtual addresses,
@@ -207,23 +227,21 @@ typedef struct hm_seg_chunk hm_seg_chunk;
 /* Gradient reduce-scatter of the owned pages fused with the layer's finite
  * flag and squared norm: local[off] = rn16(sum_r peer_r[off]) in f32, rank
  * order 0..N-1 (P2P loads), or the switch's sum (mc_pool != NULL: NVLS
- * multimem.ld_reduce).  chunks: owned pool segments, slot = layer. */
+ * multimem.ld_reduce).  chunks: owned pool segments, slot = layer.
+ * opts: grid_ctas (0 = one CTA per chunk; > 0 = a persistent grid striding
+ * over the chunks, so the reduce of one layer group can share the SMs with
+ * the page-Adam of the previous group), reduce_width, reduce_wide. */
 int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_pool,
                        void* local_pool, int dtype, const hm_seg_chunk* chunks, int64_t n_chunks,
-                       uint32_t* nonfinite, double* sumsq, void* stream);
-/* Grid of hm_dp_reduce_check: 0 (default) = one CTA per chunk; ctas > 0 = a
- * persistent grid of that many CTAs striding over the chunks, so the reduce
- * of one layer group can share the SMs with the page-Adam of the previous
- * group (layer-group pipelined DP step).  Process-wide. */
+                       uint32_t* nonfinite, double* sumsq, const hm_launch_opts* opts, void* stream);
+/* Process-wide DEFAULTS of hm_launch_opts.grid_ctas / reduce_width /
+ * reduce_wide for hm_dp_reduce_check: persistent grid (0 = one CTA per
+ * chunk); minimum peer-array width (0 = the peer count rounded up to
+ * 2/4/8; 8 exercises the N=8 instantiation on a 2- or 4-GPU box, same
+ * results at every width); 1 (default) = 32 B per thread and peer (256-bit
+ * loads; fewer read requests on the reverse link), 0 = 16 B loads. */
 int hm_set_dp_reduce_ctas(int ctas);
-/* Minimum peer-array width (0 = the peer count rounded up to 2/4/8) of the
- * reduce kernel, so the 8-wide instantiation can be exercised on a 2- or
- * 4-GPU box.  Same results at every width.  Process-wide. */
 int hm_set_dp_reduce_width(int width);
-/* 1 (default): hm_dp_reduce_check pulls 32 B per thread and peer (256-bit
- * loads, 16 elements; fewer read requests on the reverse link direction);
- * 0: 16 B loads.  Same bits either way (the persistent grid always uses the
- * 16 B form).  Process-wide. */
 int hm_set_dp_reduce_wide(int wide);
 /* flags_out[l] = OR_r peer_flags_r[l]; sumsq_out[l] = sum_r peer_sumsq_r[l]
  * (rank order).  Replaces an all-reduce of the per-layer reject flags. */
@@ -236,18 +254,15 @@ int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_grou
                     const hm_group_rt* rt, const void* g, int g_dtype,
                     float* p32, float* m32, float* v32,
                     const uint64_t* peer_p16, int n_peers, void* mc_p16, int p16_dtype,
-                    const hm_adam_hyper* hyper, void* stream);
-/* Publish epilogue of hm_adam_main_ag over P2P (no multicast): 0 = every
- * thread stores its 16 B granules into every peer (default); 1 = the CTA
- * stages its 16-bit chunk in shared memory and one thread pushes it to every
- * peer with cp.async.bulk; 2 = as 1, the CTA also waits for the remote
- * writes to complete before it retires.  Same bytes, same results.
- * Process-wide. */
+                    const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream);
+/* Process-wide DEFAULTS of hm_launch_opts.ag_publish / grid_ctas for
+ * hm_adam_main_ag.  Publish epilogue over P2P: 0 = every thread stores its
+ * 16 B granules into every peer (default); 1 (or 2) = the CTA stages its
+ * 16-bit chunk in shared memory, one thread pushes it to every peer with
+ * cp.async.bulk and waits for the remote writes before the CTA retires.
+ * Grid (per-thread stores or multicast): 0 = one CTA per chunk; > 0 = a
+ * persistent grid striding over the chunks. */
 int hm_set_ag_publish(int mode);
-/* Grid of hm_adam_main_ag (per-thread peer stores or multicast): 0 (default)
- * = one CTA per chunk; ctas > 0 = a persistent grid striding over the chunks,
- * so the update of one layer group takes a fixed share of the SMs beside the
- * persistent reduce of the next.  Process-wide. */
 int hm_set_dp_update_ctas(int ctas);
 
 /* Elementwise segment chunk used by accumulate / cast / reduce. */
@@ -266,10 +281,25 @@ typedef struct hm_seg_chunk {
  * sumsq[slot] += sum(dst^2) (f64) — the layer's reject flag
  * (lockfree.py:133) and grad-norm term, so the update never re-reads g.
  * slot_modes (nullable): per-slot mode overriding `mode`, so one launch can
- * accumulate a whole flat gradient into many layers' pages. */
+ * accumulate a whole flat gradient into many layers' pages.
+ * Ledger (nullable, ConservationLedger, lockfree.py:218-222, 275-326):
+ * lsum[slot] += f64 sum(new - old) — the buffer's running f64 sum, read and
+ * reset at the take — and, if ldelta != NULL, ldelta[slot] += the same
+ * value: this message's produced delta (ldelta is a zeroed row per launch).
+ * opts: reserved (one launch shape; pass NULL). */
 int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
                   const hm_seg_chunk* chunks, int64_t n_chunks, int mode,
-                  const uint8_t* slot_modes, uint32_t* nonfinite, double* sumsq, void* stream);
+                  const uint8_t* slot_modes, uint32_t* nonfinite, double* sumsq,
+                  double* lsum, double* ldelta, const hm_launch_opts* opts, void* stream);
+
+/* The take of a gradient buffer's fused statistics (ParamBuffer.take /
+ * publish(clear=True) hand-over, lockfree.py:226-241, 251-256): for each
+ * slots[i] (device array), out[2i] = lsum[slot] (ledger record_take sum)
+ * and out[2i+1] = nonfinite[slot] as a double; then nonfinite, sumsq and
+ * lsum of the slot are reset to zero.  Any of nonfinite / sumsq / lsum /
+ * out may be NULL. */
+int hm_stats_take(const uint32_t* slots, int32_t n_slots, uint32_t* nonfinite, double* sumsq,
+                  double* lsum, double* out, void* stream);
 
 /* RNE dtype conversion over segments: publish cast (lockfree.py:169), take
  * widen (lockfree.py:234), pack/unpack of typed tensors. */

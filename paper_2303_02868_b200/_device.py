@@ -33,6 +33,11 @@ def ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+def addr(x) -> int:
+    """Device address of a tensor, or a raw address passed through."""
+    return x if isinstance(x, int) else ptr(x)
+
+
 def cur_stream(device, stream=None):
     return stream if stream is not None else torch.cuda.current_stream(device)
 
@@ -44,12 +49,18 @@ def sptr(stream) -> C.c_void_p:
 class DescCache:
     """Device copies of host descriptor arrays.  Static plans are keyed by the
     identity of the (cached, immortal) numpy array; per-launch tables by their
-    bytes in a small LRU, so steady-state sweeps upload nothing."""
+    bytes in a small LRU, so steady-state sweeps upload nothing.
+
+    Uploads are allocated on the caller's current stream.  A table used by a
+    launch on another stream names that stream (``table(arr, stream)``):
+    when the LRU evicts the table, it is ``record_stream``-ed on every stream
+    that used it, so the caching allocator cannot hand the block to a new
+    upload while a queued kernel may still read it."""
 
     def __init__(self, device, lru: int = 64):
         self.device = device
         self._static: dict[int, tuple[np.ndarray, torch.Tensor]] = {}
-        self._lru: OrderedDict[bytes, torch.Tensor] = OrderedDict()
+        self._lru: OrderedDict[bytes, tuple[torch.Tensor, set]] = OrderedDict()
         self._lru_cap = lru
 
     def static(self, arr: np.ndarray) -> torch.Tensor:
@@ -63,16 +74,21 @@ class DescCache:
         weakref.finalize(arr, self._static.pop, key, None)
         return dev
 
-    def table(self, arr: np.ndarray) -> torch.Tensor:
+    def table(self, arr: np.ndarray, stream=None) -> torch.Tensor:
         key = arr.tobytes()
-        dev = self._lru.get(key)
-        if dev is not None:
+        hit = self._lru.get(key)
+        if hit is not None:
             self._lru.move_to_end(key)
-            return dev
-        dev = self._upload(arr)
-        self._lru[key] = dev
-        if len(self._lru) > self._lru_cap:
-            self._lru.popitem(last=False)
+            dev, users = hit
+        else:
+            dev, users = self._upload(arr), set()
+            self._lru[key] = (dev, users)
+            if len(self._lru) > self._lru_cap:
+                old, old_users = self._lru.popitem(last=False)[1]
+                for st in old_users:
+                    old.record_stream(st)
+        if stream is not None:
+            users.add(stream)
         return dev
 
     def _upload(self, arr: np.ndarray) -> torch.Tensor:
@@ -110,6 +126,14 @@ class BiasTable:
                     break
             self.dev = torch.tensor(np.array(self.rows, dtype=F32).reshape(-1), device=self.device)
         return self.dev, len(self.rows)
+
+
+def opts(**kw):
+    """ctypes pointer to an hm_launch_opts with the given fields (others -1 =
+    the process default); None when nothing is set."""
+    if not kw:
+        return None
+    return C.byref(N.LaunchOpts(**kw))
 
 
 def hyper_c(h) -> N.AdamHyperC:

@@ -37,6 +37,16 @@ assert ADAM_CHUNK.itemsize == 32 and GROUP_LAUNCH.itemsize == 24
 assert SEG_CHUNK.itemsize == 24 and COPY_DESC.itemsize == 24
 
 
+class LaunchOpts(C.Structure):
+    """hm_launch_opts: per-launch tuning; -1 = the process default."""
+    _fields_ = [("adam_threads", C.c_int32), ("adam_variant", C.c_int32), ("grid_ctas", C.c_int32),
+                ("ag_publish", C.c_int32), ("reduce_width", C.c_int32), ("reduce_wide", C.c_int32)]
+
+    def __init__(self, adam_threads=-1, adam_variant=-1, grid_ctas=-1, ag_publish=-1,
+                 reduce_width=-1, reduce_wide=-1):
+        super().__init__(adam_threads, adam_variant, grid_ctas, ag_publish, reduce_width, reduce_wide)
+
+
 class AdamHyperC(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("one_minus_beta1", C.c_float),
                 ("beta2", C.c_float), ("one_minus_beta2", C.c_float), ("eps", C.c_float),
@@ -48,6 +58,7 @@ _I64 = C.c_int64
 _I32 = C.c_int32
 _INT = C.c_int
 _I64P = C.POINTER(C.c_int64)
+_OPTS = C.POINTER(LaunchOpts)
 
 # name -> (restype, argtypes); the set of symbols declared in include/hm_page.h.
 SIGNATURES = {
@@ -72,7 +83,8 @@ SIGNATURES = {
     "hm_pt_tensor_pages": (_I64, [_P, _I64, _I64P, _I64]),
     "hm_pt_tensor_segments": (_I64, [_P, _I64, _I64P, _I64]),
     "hm_adam_step": (_INT, [_P, _I64, _P, _I32, _P, _P, _INT, _P, _P, _P, _P, _INT,
-                            C.POINTER(AdamHyperC), _P, _I64, _I64, _P, _P, _P, _P, _INT, _P]),
+                            C.POINTER(AdamHyperC), _P, _I64, _I64, _P, _P, _P, _P, _INT, _P, _P,
+                            _OPTS, _P]),
     "hm_set_adam_threads": (_INT, [_INT]),
     "hm_set_adam_variant": (_INT, [_INT]),
     "hm_set_dp_reduce_ctas": (_INT, [_INT]),
@@ -81,14 +93,15 @@ SIGNATURES = {
     "hm_set_ag_publish": (_INT, [_INT]),
     "hm_set_dp_update_ctas": (_INT, [_INT]),
     "hm_adam_prologue": (_INT, [_P, _I32, _P, C.POINTER(AdamHyperC), _P, _I64, _I64, _P, _P, _P,
-                                _P, _INT, _P]),
+                                _P, _INT, _P, _P, _P]),
     "hm_adam_main": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT,
-                            C.POINTER(AdamHyperC), _P]),
-    "hm_dp_reduce_check": (_INT, [_P, _INT, _P, _P, _INT, _P, _I64, _P, _P, _P]),
+                            C.POINTER(AdamHyperC), _OPTS, _P]),
+    "hm_dp_reduce_check": (_INT, [_P, _INT, _P, _P, _INT, _P, _I64, _P, _P, _OPTS, _P]),
     "hm_dp_flags_merge": (_INT, [_P, _P, _INT, _INT, _P, _P, _P]),
     "hm_adam_main_ag": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT, _P, _INT,
-                               C.POINTER(AdamHyperC), _P]),
-    "hm_accumulate": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P]),
+                               C.POINTER(AdamHyperC), _OPTS, _P]),
+    "hm_accumulate": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P, _P, _OPTS, _P]),
+    "hm_stats_take": (_INT, [_P, _I32, _P, _P, _P, _P, _P]),
     "hm_cast": (_INT, [_P, _INT, _P, _INT, _P, _I64, _P]),
     "hm_reduce_stats": (_INT, [_P, _INT, _P, _I64, _P, _P, _P, _P]),
     "hm_copy_runs": (_INT, [_P, _P, _P, _I64, _P]),

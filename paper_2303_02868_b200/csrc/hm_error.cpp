@@ -33,7 +33,7 @@ void hm_last_error_bytes(int64_t* requested, int64_t* available) {
   if (available) *available = g_available;
 }
 
-int hm_abi_version(void) { return 1; }
+int hm_abi_version(void) { return 2; }
 
 int hm_device_chunk_elems(void) { return HM_ADAM_CHUNK; }
 

@@ -36,7 +36,8 @@ adam_prologue(const hm_group_launch* __restrict__ groups, int n_groups,
               hm_group_rt* __restrict__ rt, hm_adam_hyper hyper,
               const float* __restrict__ bc_table, int64_t bc_len, int64_t explicit_step,
               int32_t* __restrict__ steps, uint32_t* __restrict__ applied,
-              uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq, int consume) {
+              uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq, int consume,
+              double* __restrict__ lsum, double* __restrict__ ledger_out) {
   __shared__ double red[kPrologueThreads / 32];
   __shared__ float s_gscale;
   const bool clip = hyper.max_norm > 0.f && sumsq != nullptr;
@@ -76,9 +77,14 @@ adam_prologue(const hm_group_launch* __restrict__ groups, int n_groups,
     r.apply = finite ? 1u : 0u;
     rt[i] = r;
     if (applied) applied[gl.group] = r.apply;
+    if (ledger_out) {   // ConservationLedger take/apply record (lockfree.py:237, :300)
+      ledger_out[2 * i] = lsum ? lsum[gl.flag] : 0.0;
+      ledger_out[2 * i + 1] = finite ? 1.0 : 0.0;
+    }
     if (consume) {
       if (nonfinite) nonfinite[gl.flag] = 0u;
       if (sumsq) sumsq[gl.flag] = 0.0;
+      if (lsum) lsum[gl.flag] = 0.0;
     }
   }
 }
@@ -90,12 +96,14 @@ adam_prologue(const hm_group_launch* __restrict__ groups, int n_groups,
 // thread pushes it to every peer with cp.async.bulk (one 8 KB bulk copy per
 // peer instead of 512 per-thread 16 B stores; the stores no longer occupy the
 // warps that stream the HBM state).
-constexpr int kPubLocal = 0, kPubPeers = 1, kPubMulticast = 2, kPubPeersBulk = 3,
-              kPubPeersBulkWait = 4;   // bulk + wait for the remote writes before the CTA retires
+// The bulk mode waits for the remote writes before the CTA retires
+// (hm_launch_opts.ag_publish 1 and 2 both select it).
+constexpr int kPubLocal = 0, kPubPeers = 1, kPubMulticast = 2, kPubPeersBulk = 3;
 template <int PUB>
-constexpr bool is_bulk() { return PUB == kPubPeersBulk || PUB == kPubPeersBulkWait; }
-// Process-wide tuning knobs (atomic: set from any host thread; each launch
-// reads a knob once, so a concurrent change never mixes two settings).
+constexpr bool is_bulk() { return PUB == kPubPeersBulk; }
+// Process-wide DEFAULTS of the tuning knobs (hm_set_*).  A launch takes its
+// settings from its own hm_launch_opts argument; a field < 0 (or a NULL
+// opts) falls back to these, read once per launch.
 std::atomic<int> g_ag_publish{0};   // hm_set_ag_publish: 0 per-thread stores; 1 bulk; 2 bulk + full wait
 std::atomic<int> g_update_ctas{0};  // hm_set_dp_update_ctas: 0 one CTA per chunk; >0 persistent grid
 
@@ -219,11 +227,12 @@ __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
       }
     }
     if constexpr (is_bulk<PUB>()) {
+      // every writer fences its shared stores toward the async proxy, then the barrier
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (tid == 0) {
         using T = typename Elem<PDT>::T;
         const uint32_t src = (uint32_t)__cvta_generic_to_shared(s_pub);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
         for (int r = 0; r < kMaxPeers; ++r) {
           if (r >= peers.n) break;
@@ -232,10 +241,10 @@ __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
                        ::"l"(dst), "r"(src), "r"(n * (uint32_t)sizeof(T)) : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if constexpr (PUB == kPubPeersBulkWait)
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        else
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        // Remote writes must be complete (not just read out of shared
+        // memory) before the CTA retires: the step's closing symmetric
+        // barrier is what tells the peers their pages have landed.
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
     }
   } else {
@@ -286,7 +295,6 @@ AdamFn pick_adam_ag_dt(int pub) {
     case kPubPeers: return adam_main<DT, DT, kPubPeers>;
     case kPubMulticast: return adam_main<DT, DT, kPubMulticast>;
     case kPubPeersBulk: return adam_main<DT, DT, kPubPeersBulk>;
-    case kPubPeersBulkWait: return adam_main<DT, DT, kPubPeersBulkWait>;
   }
   return nullptr;
 }
@@ -350,19 +358,25 @@ int prologue_args_ok(const hm_adam_hyper* hyper, const float* bc_table, int64_t 
     return hm_set_error(HM_ERR_INVALID, "adam prologue: steps[] required without explicit_step");
   return HM_OK;
 }
+
+// Per-launch setting: the opts field when given (>= 0), else the process default.
+int opt_or(const hm_launch_opts* o, int32_t hm_launch_opts::*field, int dflt) {
+  return o && o->*field >= 0 ? o->*field : dflt;
+}
 }  // namespace
 
 extern "C" int hm_adam_prologue(const hm_group_launch* groups, int32_t n_groups,
                                 hm_group_rt* rt_scratch, const hm_adam_hyper* hyper,
                                 const float* bc_table, int64_t bc_len, int64_t explicit_step,
                                 int32_t* steps, uint32_t* applied, uint32_t* nonfinite,
-                                double* sumsq, int consume_flags, void* stream) {
+                                double* sumsq, int consume_flags, double* lsum,
+                                double* ledger_out, void* stream) {
   if (int rc = prologue_args_ok(hyper, bc_table, bc_len, rt_scratch, n_groups, explicit_step, steps))
     return rc;
   HM_REQUIRE_PTRS("hm_adam_prologue", groups);
   hm::adam_prologue<<<1, hm::kPrologueThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       groups, n_groups, rt_scratch, *hyper, bc_table, bc_len, explicit_step, steps, applied,
-      nonfinite, sumsq, consume_flags);
+      nonfinite, sumsq, consume_flags, lsum, ledger_out);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }
@@ -370,17 +384,25 @@ extern "C" int hm_adam_prologue(const hm_group_launch* groups, int32_t n_groups,
 extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
                             const hm_group_launch* groups, const hm_group_rt* rt, const void* g,
                             int g_dtype, float* p32, float* m32, float* v32, void* p16,
-                            int p16_dtype, const hm_adam_hyper* hyper, void* stream) {
+                            int p16_dtype, const hm_adam_hyper* hyper, const hm_launch_opts* opts,
+                            void* stream) {
   if (!hyper || !rt) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: missing hyper/rt");
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_adam_main: bad chunk count %lld", (long long)n_chunks);
   const int pdt = p16 ? p16_dtype : 0;
-  const int threads = hm::g_adam_threads.load(std::memory_order_relaxed);
+  const int threads = opt_or(opts, &hm_launch_opts::adam_threads,
+                             hm::g_adam_threads.load(std::memory_order_relaxed));
+  const int variant = opt_or(opts, &hm_launch_opts::adam_variant,
+                             hm::g_adam_variant.load(std::memory_order_relaxed));
+  if (threads != 256 && threads != 512)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_main: 256 or 512 threads, got %d", threads);
+  if (variant != 0 && variant != 1)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_main: variant 0 or 1, got %d", variant);
   hm::AdamFn fn = hm::pick_adam(g_dtype, pdt, threads);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (n_chunks == 0) return HM_OK;
   HM_REQUIRE_PTRS("hm_adam_main", chunks, groups, g, p32, m32, v32);
-  if (hm::g_adam_variant.load(std::memory_order_relaxed) == 1)
+  if (variant == 1)
     return hm::launch_adam_tma(chunks, n_chunks, groups, rt, g, g_dtype, p32, m32, v32, p16, p16_dtype,
                                *hyper, static_cast<cudaStream_t>(stream));
   hm::PeerPtrs none{};
@@ -414,21 +436,22 @@ extern "C" int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks,
                                const hm_group_launch* groups, const hm_group_rt* rt, const void* g,
                                int g_dtype, float* p32, float* m32, float* v32,
                                const uint64_t* peer_p16, int n_peers, void* mc_p16, int p16_dtype,
-                               const hm_adam_hyper* hyper, void* stream) {
+                               const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream) {
   if (!hyper || !rt) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: missing hyper/rt");
   hm::PeerPtrs peers;
   if (int rc = hm::make_peers(peer_p16, n_peers, &peers)) return rc;
-  const int agp = hm::g_ag_publish.load(std::memory_order_relaxed);
+  const int agp = opt_or(opts, &hm_launch_opts::ag_publish, hm::g_ag_publish.load(std::memory_order_relaxed));
+  if (agp < 0 || agp > 2)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: publish mode 0, 1 or 2, got %d", agp);
   const int pub = mc_p16 ? hm::kPubMulticast
-                 : agp == 1 ? hm::kPubPeersBulk
-                 : agp == 2 ? hm::kPubPeersBulkWait : hm::kPubPeers;
+                 : agp >= 1 ? hm::kPubPeersBulk : hm::kPubPeers;
   hm::AdamFn fn = hm::pick_adam_ag(g_dtype, p16_dtype, pub);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: unsupported dtypes g=%d p16=%d", g_dtype, p16_dtype);
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_adam_main_ag: bad chunk count");
   if (n_chunks == 0) return HM_OK;
   HM_REQUIRE_PTRS("hm_adam_main_ag", chunks, groups, g, p32, m32, v32);
-  const int uctas = hm::g_update_ctas.load(std::memory_order_relaxed);
+  const int uctas = opt_or(opts, &hm_launch_opts::grid_ctas, hm::g_update_ctas.load(std::memory_order_relaxed));
   if (uctas > 0 && (pub == hm::kPubPeers || pub == hm::kPubMulticast)) {
     hm::AdamLoopFn lf = hm::pick_adam_ag_loop(g_dtype, pub);
     const int64_t grid = uctas < n_chunks ? uctas : n_chunks;
@@ -451,14 +474,15 @@ extern "C" int hm_adam_step(const hm_adam_chunk* chunks, int64_t n_chunks,
                             const hm_adam_hyper* hyper, const float* bc_table, int64_t bc_len,
                             int64_t explicit_step, int32_t* steps, uint32_t* applied,
                             uint32_t* nonfinite, double* sumsq, int consume_flags,
+                            double* lsum, double* ledger_out, const hm_launch_opts* opts,
                             void* stream) {
   const int pdt = p16 ? p16_dtype : 0;
   if (!hm::pick_adam(g_dtype, pdt, hm::kThreads))   // dtype check only
     return hm_set_error(HM_ERR_INVALID, "hm_adam_step: unsupported dtypes g=%d p16=%d", g_dtype, pdt);
   if (int rc = hm_adam_prologue(groups, n_groups, rt_scratch, hyper, bc_table, bc_len,
                                 explicit_step, steps, applied, nonfinite, sumsq, consume_flags,
-                                stream))
+                                lsum, ledger_out, stream))
     return rc;
   return hm_adam_main(chunks, n_chunks, groups, rt_scratch, g, g_dtype, p32, m32, v32, p16,
-                      p16_dtype, hyper, stream);
+                      p16_dtype, hyper, opts, stream);
 }

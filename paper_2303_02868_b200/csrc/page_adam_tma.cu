@@ -207,9 +207,11 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
         }
         if constexpr (kPub) smem_store8h<PDT>(st + L::kOffP16, e, pv);
       }
+      // Every writing thread orders its generic-proxy shared-memory stores
+      // before the async-proxy bulk reads of them, then the barrier.
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       consumers_sync();  // the stage holds the results
       if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (r.apply) {
           bulk_s2g(p32 + so, st + L::kOffP, n * 4, pol);
           bulk_s2g(m32 + so, st + L::kOffM, n * 4, pol);

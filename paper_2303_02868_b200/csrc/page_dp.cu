@@ -270,6 +270,7 @@ __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, in
 
 using RcFn = void (*)(const hm_seg_chunk*, int, PeerPtrs, const char*, void*, uint32_t*, double*);
 
+// Process-wide defaults; each launch's hm_launch_opts overrides them.
 std::atomic<int> g_reduce_ctas{0};   // 0: one CTA per chunk; >0: persistent grid (hm_set_dp_reduce_ctas)
 std::atomic<int> g_reduce_width{0};  // minimum peer-array width of the reduce kernel (test hook)
 std::atomic<int> g_reduce_wide{1};   // 1: 256-bit peer loads (hm_set_dp_reduce_wide), the default
@@ -328,23 +329,29 @@ extern "C" {
 
 int hm_dp_reduce_check(const uint64_t* peer_pools, int n_peers, const void* mc_pool,
                        void* local_pool, int dtype, const hm_seg_chunk* chunks, int64_t n_chunks,
-                       uint32_t* nonfinite, double* sumsq, void* stream) {
+                       uint32_t* nonfinite, double* sumsq, const hm_launch_opts* opts, void* stream) {
   hm::PeerPtrs peers;
   if (int rc = hm::make_peers(peer_pools, n_peers, &peers)) return rc;
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL)
     return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: bad chunk count");
   if (n_chunks == 0) return HM_OK;
   HM_REQUIRE_PTRS("hm_dp_reduce_check", local_pool, chunks);
-  const int rctas = hm::g_reduce_ctas.load(std::memory_order_relaxed);
+  // per-launch settings (opts field >= 0), else the process defaults
+  const int rctas = opts && opts->grid_ctas >= 0 ? opts->grid_ctas
+                                                 : hm::g_reduce_ctas.load(std::memory_order_relaxed);
+  const int minw = opts && opts->reduce_width >= 0 ? opts->reduce_width
+                                                   : hm::g_reduce_width.load(std::memory_order_relaxed);
+  const int wide = opts && opts->reduce_wide >= 0 ? opts->reduce_wide
+                                                  : hm::g_reduce_wide.load(std::memory_order_relaxed);
+  if (minw > hm::kMaxPeers)
+    return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: width %d > %d", minw, hm::kMaxPeers);
   const bool persistent = rctas > 0;
   int depth = 1;
   // template width: the peer count rounded up to 2/4/8, or wider if forced
-  // (hm_set_dp_reduce_width: runs the 8-wide kernel on a 2- or 4-GPU box)
-  const int width = n_peers > hm::g_reduce_width.load(std::memory_order_relaxed)
-                        ? n_peers : hm::g_reduce_width.load(std::memory_order_relaxed);
+  // (reduce_width: runs the 8-wide kernel on a 2- or 4-GPU box)
+  const int width = n_peers > minw ? n_peers : minw;
   hm::RcFn fn = hm::pick_rc(dtype, mc_pool != nullptr, width, persistent, &depth);
-  if (fn && !persistent && mc_pool == nullptr && hm::g_reduce_wide.load(std::memory_order_relaxed))
-    fn = hm::pick_rc_wide(dtype, width);
+  if (fn && !persistent && mc_pool == nullptr && wide) fn = hm::pick_rc_wide(dtype, width);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_reduce_check: unsupported dtype %d", dtype);
   const int64_t passes = (n_chunks + depth - 1) / depth;
   const int64_t grid = persistent && rctas < passes ? rctas : passes;

@@ -19,103 +19,171 @@ constexpr int kSegVecPer = kChunk / (kSegThreads * kVec);
 static_assert(kSegVecPer * kSegThreads * kVec == kChunk, "segment chunk geometry");
 
 // Flush of the fused statistics: warp shuffles, ONE block barrier, then one
-// atomic per CTA (per-warp f64 atomics on a few hundred layer addresses
-// serialise in L2 and cost 3x in measurement).  sumsq feeds the grad norm /
-// clip only, so its f64 atomic order is free to vary.
-__device__ __forceinline__ void flush_stats(bool bad, float sq, uint32_t* nonfinite, double* sumsq,
+// atomic per CTA and statistic (per-warp f64 atomics on a few hundred layer
+// addresses serialise in L2 and cost 3x in measurement).  sumsq feeds the
+// grad norm / clip only, so its f64 atomic order is free to vary.  The
+// ledger sum (LEDGER) is the f64 sum of (new - old) over the chunk: it goes
+// to the slot's running sum (the buffer's total, read at take) and to the
+// message's delta row (ConservationLedger.record_accumulate,
+// hiermem/lockfree.py:218-222).  REUSE: a second barrier so the CTA can
+// flush again (multi-chunk CTAs).
+template <bool LEDGER, bool REUSE>
+__device__ __forceinline__ void flush_stats(bool bad, float sq, double ls, uint32_t* nonfinite,
+                                            double* sumsq, double* lsum, double* ldelta,
                                             uint32_t slot) {
   __shared__ float s_sq[kSegThreads / 32];
   __shared__ int s_bad[kSegThreads / 32];
+  __shared__ double s_ls[LEDGER ? kSegThreads / 32 : 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if constexpr (LEDGER) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+  }
   const int any = __any_sync(0xffffffffu, bad);
   if (lane == 0) {
     s_sq[warp] = sq;
     s_bad[warp] = any;
+    if constexpr (LEDGER) s_ls[warp] = ls;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     float t = 0.f;
+    double l = 0.0;
     int b = 0;
 #pragma unroll
     for (int w = 0; w < kSegThreads / 32; ++w) {
       t += s_sq[w];
       b |= s_bad[w];
+      if constexpr (LEDGER) l += s_ls[w];
     }
     if (nonfinite && b) atomicOr(&nonfinite[slot], 1u);
     if (sumsq && t != 0.f) atomicAdd(&sumsq[slot], (double)t);
+    if constexpr (LEDGER) {
+      if (l != 0.0 || l != l) {   // NaN must propagate (a poisoned ledger is unbalanced)
+        atomicAdd(&lsum[slot], l);
+        if (ldelta) atomicAdd(&ldelta[slot], l);
+      }
+    }
   }
+  if constexpr (REUSE) __syncthreads();
 }
+
+// Per-thread ledger accumulator.  LM 1: f64 adds per element (every
+// widening conversion on the FP64 path); LM 2: compensated f32 (Neumaier:
+// running sum + f32 error term, both widened to f64 once per flush).  For
+// 16-bit inputs of a realistic range both are exact, so the device sums
+// equal the reference's np.sum(g16, dtype=float64) (tests/test_gpu_toy_sync.py).
+template <int LM>
+struct LedgerAcc;
+template <>
+struct LedgerAcc<0> {
+  __device__ __forceinline__ void add(float) {}
+  __device__ __forceinline__ void add_delta(float, float) {}
+  __device__ __forceinline__ double total() const { return 0.0; }
+  __device__ __forceinline__ void reset() {}
+};
+template <>
+struct LedgerAcc<1> {
+  double s = 0.0;
+  __device__ __forceinline__ void add(float x) { s += (double)x; }
+  __device__ __forceinline__ void add_delta(float r, float b) { s += (double)r - (double)b; }
+  __device__ __forceinline__ double total() const { return s; }
+  __device__ __forceinline__ void reset() { s = 0.0; }
+};
+template <>
+struct LedgerAcc<2> {
+  float s = 0.f, c = 0.f;
+  __device__ __forceinline__ void add(float x) {
+    const float t = __fadd_rn(s, x);
+    c = __fadd_rn(c, fabsf(s) >= fabsf(x) ? __fadd_rn(__fsub_rn(s, t), x) : __fadd_rn(__fsub_rn(x, t), s));
+    s = t;
+  }
+  __device__ __forceinline__ void add_delta(float r, float b) {
+    add(r);
+    add(-b);
+  }
+  __device__ __forceinline__ double total() const { return (double)s + (double)c; }
+  __device__ __forceinline__ void reset() { s = c = 0.f; }
+};
+
 
 // dst = rn(f32(dst) + f32(src)) (add) or rn(0.0f + f32(src)) (first message).
 // sumsq accumulates sum(new^2 - old^2) so that it telescopes to the squared
-// norm of the final buffer over any number of messages.
+// norm of the final buffer over any number of messages; the ledger sum
+// likewise accumulates sum(new - old).
+//
+// One 4096-element chunk per CTA, every raw load of the thread issued before
+// any decode.  KIND: 0 = every chunk is a first message (the common case:
+// one message per step; only the source is read, 16 data registers, so 32
+// registers per thread and 16 CTAs = 64 warps per SM — ncu on C2: register-
+// limited occupancy (40 warps) left the loads latency-bound at 60% of DRAM
+// peak); 1 = every chunk adds; 2 = per-slot mode from slot_modes.  More
+// chunks per CTA with the same bytes in flight measured 50% slower (fewer
+// resident CTAs to overlap the store and epilogue phases).
 template <int SDT, int DDT>
-__global__ void __launch_bounds__(kSegThreads)
+constexpr int acc_min_blocks(int kind) {
+  // f32 granules are 32 B (twice the registers of a 16-bit granule)
+  return SDT == HM_DT_F32 || DDT == HM_DT_F32 ? (kind == 0 ? 8 : 4) : (kind == 0 ? 16 : 8);
+}
+
+template <int SDT, int DDT, int KIND, int LM>
+__global__ void __launch_bounds__(kSegThreads, acc_min_blocks<SDT, DDT>(KIND))
 accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
-                  void* __restrict__ dst, int mode, const uint8_t* __restrict__ slot_modes,
-                  uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq) {
+                  void* __restrict__ dst, const uint8_t* __restrict__ slot_modes,
+                  uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq,
+                  double* __restrict__ lsum, double* __restrict__ ldelta) {
+  constexpr bool LEDGER = LM != 0;
   const hm_seg_chunk c = chunks[blockIdx.x];
-  const int add = slot_modes ? (int)slot_modes[c.slot] : mode;
+  const bool add = KIND == 1 || (KIND == 2 && slot_modes[c.slot] != 0);
   const int tid = threadIdx.x;
   bool bad = false;
   float sq = 0.f;
+  LedgerAcc<LM> ls;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
   if (vec) {
-    // All raw loads first (one straight-line batch per mode), decode after.
     Raw8<SDT> ra[kSegVecPer];
-    Raw8<DDT> rb[kSegVecPer];
-    if (add) {
+    Raw8<DDT> rb[KIND == 0 ? 1 : kSegVecPer];
 #pragma unroll
-      for (int k = 0; k < kSegVecPer; ++k) {
-        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-        if (e < c.n) {
-          ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
-          ld_raw_rw<DDT>(dst, c.dst_off + e, rb[k]);
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
+      if (e < c.n) {
+        ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
+        if constexpr (KIND != 0) {
+          if (add) ld_raw_rw<DDT>(dst, c.dst_off + e, rb[k]);
         }
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < kSegVecPer; ++k) {
-        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-        if (e < c.n) ld_raw_ro<SDT>(src, c.src_off + e, ra[k]);
-      }
     }
-    if (add) {
 #pragma unroll
-      for (int k = 0; k < kSegVecPer; ++k) {
-        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-        if (e >= c.n) continue;
-        F8 a, b, o;
-        decode<SDT>(ra[k], a);
-        decode<DDT>(rb[k], b);
+    for (int k = 0; k < kSegVecPer; ++k) {
+      const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
+      if (e >= c.n) continue;
+      F8 a, o;
+      decode<SDT>(ra[k], a);
+      if (KIND != 0 && add) {
+        F8 b;
+        decode<DDT>(rb[KIND == 0 ? 0 : k], b);
 #pragma unroll
         for (int j = 0; j < kVec; ++j) {
           const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b.v[j], a.v[j])));
           bad |= !is_finite(r);
-          if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b.v[j], b.v[j]));
+          sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b.v[j], b.v[j]));
+          if constexpr (LEDGER) ls.add_delta(r, b.v[j]);
           o.v[j] = r;
         }
-        store8<DDT>(dst, c.dst_off + e, o);
-      }
-    } else {   // first message after a take: the buffer holds zeros, r = 0 + a
-#pragma unroll
-      for (int k = 0; k < kSegVecPer; ++k) {
-        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * kVec;
-        if (e >= c.n) continue;
-        F8 a, o;
-        decode<SDT>(ra[k], a);
+      } else {   // first message after a take: the buffer holds zeros, r = 0 + a
 #pragma unroll
         for (int j = 0; j < kVec; ++j) {
           // 0 + a keeps the reference's -0 -> +0; r*r - 0*0 == r*r exactly
           const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(0.0f, a.v[j])));
           bad |= !is_finite(r);
-          if (sumsq) sq += __fmul_rn(r, r);
+          sq += __fmul_rn(r, r);
+          if constexpr (LEDGER) ls.add(r);
           o.v[j] = r;
         }
-        store8<DDT>(dst, c.dst_off + e, o);
       }
+      store8<DDT>(dst, c.dst_off + e, o);
     }
   } else {
     for (uint32_t i = tid; i < c.n; i += kSegThreads) {
@@ -123,11 +191,32 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
       const float b1 = add ? load1<DDT>(dst, c.dst_off + i) : 0.0f;
       const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(b1, a1)));
       bad |= !is_finite(r);
-      if (sumsq) sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b1, b1));
+      sq += __fsub_rn(__fmul_rn(r, r), __fmul_rn(b1, b1));
+      if constexpr (LEDGER) ls.add_delta(r, b1);
       store1<DDT>(dst, c.dst_off + i, r);
     }
   }
-  flush_stats(bad, sq, nonfinite, sumsq, c.slot);
+  flush_stats<LEDGER, false>(bad, sq, ls.total(), nonfinite, sumsq, lsum, ldelta, c.slot);
+}
+
+// Snapshot-and-clear of a gradient buffer's fused statistics at a take
+// (hiermem/lockfree.py:226-241 hand-over): out[2i] = running ledger sum,
+// out[2i+1] = non-finite flag of slot slots[i]; then the slot's flag, norm
+// and ledger sum are reset for the buffer's next first message.  Any
+// pointer may be NULL (out NULL: reset only).
+__global__ void stats_take_kernel(const uint32_t* __restrict__ slots, int n,
+                                  uint32_t* __restrict__ nonfinite, double* __restrict__ sumsq,
+                                  double* __restrict__ lsum, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t s = slots[i];
+    if (out) {
+      out[2 * i] = lsum ? lsum[s] : 0.0;
+      out[2 * i + 1] = nonfinite ? (double)nonfinite[s] : 0.0;
+    }
+    if (nonfinite) nonfinite[s] = 0u;
+    if (sumsq) sumsq[s] = 0.0;
+    if (lsum) lsum[s] = 0.0;
+  }
 }
 
 template <int SDT, int DDT>
@@ -202,7 +291,7 @@ reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ 
     const double tot = block_sum<kSegThreads>(s, red);
     if (threadIdx.x == 0) atomicAdd(&sums[c.slot], tot);
   }
-  flush_stats(bad, (float)sq, nonfinite, sumsq, c.slot);
+  flush_stats<false, false>(bad, (float)sq, 0.0, nonfinite, sumsq, nullptr, nullptr, c.slot);
 }
 
 // Occupies one warp of the stream for `ns` nanoseconds of %globaltimer: the
@@ -277,25 +366,42 @@ copy_runs_kernel(const char* __restrict__ src, char* __restrict__ dst,
 }
 
 
-using AccFn = void (*)(const hm_seg_chunk*, const void*, void*, int, const uint8_t*, uint32_t*,
-                       double*);
+using AccFn = void (*)(const hm_seg_chunk*, const void*, void*, const uint8_t*, uint32_t*, double*,
+                       double*, double*);
 using CastFn = void (*)(const hm_seg_chunk*, const void*, void*);
 using RedFn = void (*)(const hm_seg_chunk*, const void*, uint32_t*, double*, double*);
 
+// Ledger accumulator per kernel form (measured on C2, bf16): first messages
+// with the compensated f32 sum run at 0.86-0.88 ms (f64 per element: 1.03
+// ms — the widening conversions, not the memory, become the limit); adds
+// (two terms per element) with f64 at 1.20 ms (compensated f32: 1.49 ms).
+template <int S, int D, int K>
+AccFn acc_k(bool ledger) {
+  if (!ledger) return accumulate_kernel<S, D, K, 0>;
+  return accumulate_kernel<S, D, K, K == 0 ? 2 : 1>;
+}
+template <int S, int D>
+AccFn acc_sd(int kind, bool ledger) {
+  switch (kind) {
+    case 0: return acc_k<S, D, 0>(ledger);
+    case 1: return acc_k<S, D, 1>(ledger);
+    default: return acc_k<S, D, 2>(ledger);
+  }
+}
 template <int S>
-AccFn acc_d(int d) {
+AccFn acc_d(int d, int kind, bool ledger) {
   switch (d) {
-    case HM_DT_F16: return accumulate_kernel<S, HM_DT_F16>;
-    case HM_DT_BF16: return accumulate_kernel<S, HM_DT_BF16>;
-    case HM_DT_F32: return accumulate_kernel<S, HM_DT_F32>;
+    case HM_DT_F16: return acc_sd<S, HM_DT_F16>(kind, ledger);
+    case HM_DT_BF16: return acc_sd<S, HM_DT_BF16>(kind, ledger);
+    case HM_DT_F32: return acc_sd<S, HM_DT_F32>(kind, ledger);
   }
   return nullptr;
 }
-AccFn pick_acc(int s, int d) {
+AccFn pick_acc(int s, int d, int kind, bool ledger) {
   switch (s) {
-    case HM_DT_F16: return acc_d<HM_DT_F16>(d);
-    case HM_DT_BF16: return acc_d<HM_DT_BF16>(d);
-    case HM_DT_F32: return acc_d<HM_DT_F32>(d);
+    case HM_DT_F16: return acc_d<HM_DT_F16>(d, kind, ledger);
+    case HM_DT_BF16: return acc_d<HM_DT_BF16>(d, kind, ledger);
+    case HM_DT_F32: return acc_d<HM_DT_F32>(d, kind, ledger);
   }
   return nullptr;
 }
@@ -338,14 +444,31 @@ extern "C" {
 
 int hm_accumulate(const void* src, int src_dtype, void* dst, int dst_dtype,
                   const hm_seg_chunk* chunks, int64_t n_chunks, int mode,
-                  const uint8_t* slot_modes, uint32_t* nonfinite, double* sumsq, void* stream) {
+                  const uint8_t* slot_modes, uint32_t* nonfinite, double* sumsq,
+                  double* lsum, double* ldelta, const hm_launch_opts* opts, void* stream) {
+  (void)opts;   // one launch shape (see accumulate_kernel)
   if (int rc = hm::check_grid(n_chunks, "hm_accumulate")) return rc;
-  hm::AccFn fn = hm::pick_acc(src_dtype, dst_dtype);
+  if (ldelta && !lsum)
+    return hm_set_error(HM_ERR_INVALID, "hm_accumulate: a ledger delta row needs the running sums");
+  const int kind = slot_modes ? 2 : mode ? 1 : 0;
+  hm::AccFn fn = hm::pick_acc(src_dtype, dst_dtype, kind, lsum != nullptr);
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_accumulate: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
   if (n_chunks == 0) return HM_OK;
   HM_REQUIRE_PTRS("hm_accumulate", src, dst, chunks);
   fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      chunks, src, dst, mode ? 1 : 0, slot_modes, nonfinite, sumsq);
+      chunks, src, dst, slot_modes, nonfinite, sumsq, lsum, ldelta);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_stats_take(const uint32_t* slots, int32_t n_slots, uint32_t* nonfinite, double* sumsq,
+                  double* lsum, double* out, void* stream) {
+  if (n_slots < 0) return hm_set_error(HM_ERR_INVALID, "hm_stats_take: negative slot count");
+  if (n_slots == 0) return HM_OK;
+  HM_REQUIRE_PTRS("hm_stats_take", slots);
+  const int blocks = (n_slots + 255) / 256;
+  hm::stats_take_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(slots, n_slots, nonfinite,
+                                                                               sumsq, lsum, out);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }

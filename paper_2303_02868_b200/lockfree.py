@@ -27,6 +27,7 @@ callers), torch in → CUDA tensors out.
 from __future__ import annotations
 
 import math
+import weakref
 from collections.abc import Sequence
 from dataclasses import dataclass
 
@@ -108,38 +109,98 @@ class GradMessage:
     iteration: int
 
 
+class _Pending:
+    """A ledger entry still sitting in a device ledger row (resolved lazily)."""
+
+    __slots__ = ("row", "col")
+
+    def __init__(self, row: int, col: int):
+        self.row, self.col = row, col
+
+
 class ConservationLedger:
     """Gradient conservation bookkeeping (hiermem/lockfree.py:275-326):
     per-layer f64 produced deltas, consumed and applied sums and message
     counts; balanced iff fsum(produced) == fsum(consumed) == fsum(applied +
-    rejected) and the counts agree.  Sums are device f64 reductions, so they
-    are recorded only when the owning buffer was built with ``ledger=True``."""
+    rejected) and the counts agree.
+
+    Always on, like the reference's.  The sums are not separate passes: the
+    accumulate kernel (K3) folds the f64 sum of (new - old) of every message
+    into the same HBM pass, into a per-slot running sum (the buffer's total)
+    and into the message's row of a device ledger ring; the take (prologue of
+    the fused update, or hm_stats_take) snapshots and resets the running sum.
+    Entries stay on the device until someone reads the ledger (``summary()``
+    or the list attributes), so the update path never synchronises for it."""
 
     def __init__(self, num_layers: int):
-        self.produced_deltas = [[] for _ in range(num_layers)]
-        self.consumed_sums = [[] for _ in range(num_layers)]
-        self.applied_sums = [[] for _ in range(num_layers)]
-        self.rejected_sums = [[] for _ in range(num_layers)]
+        self._produced = [[] for _ in range(num_layers)]
+        self._consumed = [[] for _ in range(num_layers)]
+        self._applied = [[] for _ in range(num_layers)]
+        self._rejected = [[] for _ in range(num_layers)]
+        self._apply_pending: list[tuple[int, int, int, int]] = []   # (layer, row, sum col, flag col)
+        self._unresolved: list[tuple[list, int, int, int]] = []     # (entries, index, row, col)
         self.messages_sent = [0] * num_layers
         self.messages_accumulated = [0] * num_layers
         self.messages_consumed = [0] * num_layers
+        self._resolver = None   # ParamBuffer._ledger_flush: device rows -> floats
+
+    def _sync(self):
+        if self._resolver is not None:
+            self._resolver()
+
+    def _pend(self, entries: list, row: int, col: int) -> None:
+        """Append an entry that a device ledger row will fill in."""
+        self._unresolved.append((entries, len(entries), row, col))
+        entries.append(_Pending(row, col))
+
+    def _resolve(self, host: np.ndarray) -> None:
+        for entries, i, row, col in self._unresolved:
+            entries[i] = float(host[row, col])
+        self._unresolved.clear()
+        for layer, row, cs, cf in self._apply_pending:
+            (self._applied if host[row, cf] != 0.0 else self._rejected)[layer].append(float(host[row, cs]))
+        self._apply_pending.clear()
+
+    @property
+    def produced_deltas(self):
+        self._sync()
+        return self._produced
+
+    @property
+    def consumed_sums(self):
+        self._sync()
+        return self._consumed
+
+    @property
+    def applied_sums(self):
+        self._sync()
+        return self._applied
+
+    @property
+    def rejected_sums(self):
+        self._sync()
+        return self._rejected
 
     def record_accumulate(self, layer: int, delta: float) -> None:
-        self.produced_deltas[layer].append(delta)
+        self._sync()
+        self._produced[layer].append(delta)
         self.messages_accumulated[layer] += 1
 
     def record_take(self, layer: int, total: float, count: int) -> None:
-        self.consumed_sums[layer].append(total)
+        self._sync()
+        self._consumed[layer].append(total)
         self.messages_consumed[layer] += count
 
     def record_apply(self, layer: int, total: float, rejected: bool) -> None:
-        (self.rejected_sums if rejected else self.applied_sums)[layer].append(total)
+        self._sync()
+        (self._rejected if rejected else self._applied)[layer].append(total)
 
     def summary(self) -> dict:
+        self._sync()
         out, balanced = [], True
-        for l in range(len(self.produced_deltas)):
-            sums = [math.fsum(x) for x in (self.produced_deltas[l], self.consumed_sums[l],
-                                            self.applied_sums[l], self.rejected_sums[l])]
+        for l in range(len(self._produced)):
+            sums = [math.fsum(x) for x in (self._produced[l], self._consumed[l],
+                                            self._applied[l], self._rejected[l])]
             ok = (sums[0] == sums[1] == sums[2] + sums[3]
                   and self.messages_accumulated[l] == self.messages_consumed[l] == self.messages_sent[l])
             balanced &= ok
@@ -160,8 +221,29 @@ def _shape(x):
     return tuple(x.shape) if hasattr(x, "shape") else tuple(np.shape(x))
 
 
+class _StreamScratch:
+    """Device scratch of ONE stream: the prologue's per-group runtime table
+    and the reject flag of update_layer.  Allocated on that stream, so the
+    caching allocator orders any reuse behind the stream's own kernels, and
+    launches on other streams never share it."""
+
+    def __init__(self, device, stream):
+        self.device, self.stream = device, stream
+        with torch.cuda.stream(stream):
+            self.rt = torch.empty(64 * N.GROUP_RT_BYTES, dtype=torch.uint8, device=device)
+            self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def rt_for(self, n_groups: int) -> torch.Tensor:
+        need = max(1, n_groups) * N.GROUP_RT_BYTES
+        if self.rt.numel() < need:
+            with torch.cuda.stream(self.stream):
+                self.rt = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self.rt
+
+
 class _Engine:
-    """Per-device descriptor cache, rt scratch and bias tables."""
+    """Per-device descriptor cache and bias tables (read-only after build),
+    plus per-stream scratch."""
 
     _per_device: dict = {}
 
@@ -169,9 +251,7 @@ class _Engine:
         self.device = device
         self.desc = D.DescCache(device)
         self.bias: dict[tuple[float, float], D.BiasTable] = {}
-        self.rt = torch.empty(0, dtype=torch.uint8, device=device)
-        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
-        self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
+        self._scratch: dict[int, _StreamScratch] = {}
 
     @classmethod
     def of(cls, device) -> "_Engine":
@@ -180,11 +260,15 @@ class _Engine:
             cls._per_device[key] = cls(device)
         return cls._per_device[key]
 
-    def rt_scratch(self, n_groups: int) -> torch.Tensor:
-        need = max(1, n_groups) * N.GROUP_RT_BYTES
-        if self.rt.numel() < need:
-            self.rt = torch.empty(need, dtype=torch.uint8, device=self.device)
-        return self.rt
+    def scratch(self, stream) -> _StreamScratch:
+        key = int(stream.cuda_stream)
+        sc = self._scratch.get(key)
+        if sc is None or sc.stream != stream:
+            sc = self._scratch[key] = _StreamScratch(self.device, stream)
+        return sc
+
+    def rt_scratch(self, n_groups: int, stream) -> torch.Tensor:
+        return self.scratch(stream).rt_for(n_groups)
 
     def bias_table(self, hyper, max_step: int):
         key = (float(hyper.beta1), float(hyper.beta2))
@@ -196,17 +280,21 @@ class _Engine:
 def adam_launch(engine: _Engine, chunks: np.ndarray, groups: np.ndarray, g, g_dt: int,
                 p32, m32, v32, p16, p16_dt: int, hyper, bc_dev, bc_len: int,
                 explicit_step: int, steps, applied, nonfinite, sumsq, consume: bool, stream,
-                static_chunks: bool = True) -> None:
-    """One fused page-Adam step (prologue + main kernel) on ``stream``."""
-    dchunks = engine.desc.static(chunks) if static_chunks else engine.desc.table(chunks)
-    dgroups = engine.desc.table(groups)
-    rt = engine.rt_scratch(len(groups))
+                static_chunks: bool = True, lsum: int = 0, ledger_out: int = 0, opts=None) -> None:
+    """One fused page-Adam step (prologue + main kernel) on ``stream``.
+    ``steps`` / ``applied`` / ``nonfinite`` / ``sumsq`` are tensors or raw
+    device addresses (int); ``lsum`` / ``ledger_out`` raw addresses."""
+    dchunks = engine.desc.static(chunks) if static_chunks else engine.desc.table(chunks, stream)
+    dgroups = engine.desc.table(groups, stream)
+    rt = engine.rt_scratch(len(groups), stream)
     hc = D.hyper_c(hyper)
+    a = D.addr
     D.check(N.lib().hm_adam_step(
         D.ptr(dchunks), len(chunks), D.ptr(dgroups), len(groups), D.ptr(rt),
         D.ptr(g), g_dt, D.ptr(p32), D.ptr(m32), D.ptr(v32), D.ptr(p16), p16_dt,
-        hc, D.ptr(bc_dev), bc_len, explicit_step, D.ptr(steps), D.ptr(applied),
-        D.ptr(nonfinite), D.ptr(sumsq), 1 if consume else 0, D.sptr(stream)))
+        hc, D.ptr(bc_dev), bc_len, explicit_step, a(steps), a(applied),
+        a(nonfinite), a(sumsq), 1 if consume else 0, lsum or None, ledger_out or None, opts,
+        D.sptr(stream)))
 
 
 def _group_rows(rows) -> np.ndarray:
@@ -214,6 +302,32 @@ def _group_rows(rows) -> np.ndarray:
     for i, (gs, ps, grp, flag) in enumerate(rows):
         a[i] = (gs, ps, grp, flag)
     return a
+
+
+class Applied:
+    """Lazy result of ``MasterState.update_layer`` for torch callers: the
+    update is queued on the stream; the bool is read (one synchronisation)
+    only when the caller asks for it — ``bool(x)``, ``x == True``."""
+
+    __slots__ = ("_t", "_stream", "_v")
+
+    def __init__(self, t: torch.Tensor, stream):
+        self._t, self._stream, self._v = t, stream, None
+
+    def __bool__(self) -> bool:
+        if self._v is None:
+            with torch.cuda.stream(self._stream):
+                self._v = bool(self._t.item())
+        return self._v
+
+    def __eq__(self, other):
+        return bool(self) == other
+
+    def __hash__(self):
+        return hash(bool(self))
+
+    def __repr__(self):
+        return repr(bool(self))
 
 
 # ---- functional update (hiermem/lockfree.py:127-142) ------------------------------
@@ -243,8 +357,8 @@ def apply_update(p32, m32, v32, grad, hyper: AdamHyper, step: int, *, stream=Non
                            float(np.float32(1.0 - hyper.beta2 ** step))], dtype=torch.float32, device=device)
         flag = torch.zeros(1, dtype=torch.int32, device=device)
         applied = torch.zeros(1, dtype=torch.int32, device=device)
-    D.check(N.lib().hm_reduce_stats(D.ptr(g), D.DT_OF_TORCH[g.dtype],
-                                     D.ptr(eng.desc.static(D.contiguous_chunks_cached(n))), len(D.contiguous_chunks_cached(n)),
+    cc = D.contiguous_chunks_cached(n)
+    D.check(N.lib().hm_reduce_stats(D.ptr(g), D.DT_OF_TORCH[g.dtype], D.ptr(eng.desc.static(cc)), len(cc),
                                      D.ptr(flag), None, None, D.sptr(st)))
     adam_launch(eng, D.contiguous_adam_chunks(n), _group_rows([(0, 0, 0, 0)]), g, D.DT_OF_TORCH[g.dtype],
                 p, m, v, None, 0, hyper, bc, 1, int(step), None, applied, flag, None, True, st,
@@ -324,6 +438,19 @@ class _Paged:
 
 # ---- MasterState (hiermem/lockfree.py:145-165) ---------------------------------------
 
+class _Taken:
+    """Tag on the f32 tensor ``ParamBuffer.take`` returns to a torch caller:
+    where its 16-bit source pages are, so ``update_layer`` can read them in
+    place (2 B/param) and reuse the reject flag K3 already computed, as long
+    as the tensor is unmodified (``_version``) and its pages were not taken
+    again."""
+
+    __slots__ = ("buffer", "layer", "gbuf", "version")
+
+    def __init__(self, buffer, layer, gbuf, version):
+        self.buffer, self.layer, self.gbuf, self.version = weakref.ref(buffer), layer, gbuf, version
+
+
 class MasterState(_Paged):
     """FP32 masters (params, moments) per layer in fp32 page pools; mutated
     only by the updater.  ``tier`` is the reference's label (:148); the
@@ -342,13 +469,14 @@ class MasterState(_Paged):
             self._steps = torch.zeros(self.num_layers, dtype=torch.int32, device=self.device)
             self._applied = torch.zeros(self.num_layers, dtype=torch.int32, device=self.device)
         self._step_bound = [0] * self.num_layers
+        self._prepub = [None] * self.num_layers   # (buffer ref, token) of a pre-published p16
         for l, p in enumerate(params):
             self._pack_p32(l, p, st)
 
     # reference attributes ------------------------------------------------------
     @property
     def p32(self):
-        return _LayerView(self, lambda l: self._unpack(self.p32_pool, l), self._pack_p32)
+        return _LayerView(self, self._p32_of, self._pack_p32)
 
     @property
     def m32(self):
@@ -362,7 +490,18 @@ class MasterState(_Paged):
     def steps(self) -> list[int]:
         return [int(x) for x in self._steps.cpu().tolist()]
 
+    def _p32_of(self, layer):
+        out = self._unpack(self.p32_pool, layer)
+        if isinstance(out, torch.Tensor) and self._prepub[layer] is not None:
+            # the fast update_layer already cast these values into the
+            # buffer's inactive publish pages: publish() of this unmodified
+            # tensor only has to flip the record
+            bref, token = self._prepub[layer]
+            out._hm_prepub = (bref, token, layer, out._version)
+        return out
+
     def _pack_p32(self, layer, value, stream=None):
+        self._prepub[layer] = None
         st = self._stream(stream)
         with torch.cuda.stream(st):
             src = D.to_device_flat(value, self.device)
@@ -384,31 +523,81 @@ class MasterState(_Paged):
             self._step_bound[l] += 1
         return self._eng.bias_table(hyper, max(self._step_bound))
 
-    def update_layer(self, layer: int, grad, hyper: AdamHyper, *, stream=None) -> bool:
+    def _same_pages(self, lay: PageLayout) -> bool:
+        a = self.layout
+        return a is lay or (a.numels == lay.numels and a.page_bytes == lay.page_bytes
+                            and a.world_size == lay.world_size and a.rank == lay.rank and a.K == lay.K)
+
+    def update_layer(self, layer: int, grad, hyper: AdamHyper, *, stream=None):
         """steps += 1; Adam over the layer's pages; on reject steps -= 1
-        (lockfree.py:155-165).  Synchronous bool result like the reference."""
+        (lockfree.py:155-165).  numpy callers get the reference's synchronous
+        bool; torch callers an ``Applied`` that synchronises only when read.
+
+        A gradient tensor fresh from ``ParamBuffer.take`` is not re-read: the
+        update streams its 16-bit source pages (g 2 B instead of 4 B/param),
+        reuses the reject flag and norm its accumulate computed (no extra
+        isfinite pass), and casts the new masters into the buffer's inactive
+        publish pages, so the ``publish`` that follows is a record flip."""
         self._check_layer(layer)
         st = self._stream(stream)
+        self._prepub[layer] = None
+        h = getattr(grad, "_hm_taken", None) if isinstance(grad, torch.Tensor) else None
+        if h is not None:
+            buf = h.buffer()
+            if (buf is not None and h.layer == layer and grad._version == h.version
+                    and buf._gsel[layer] != h.gbuf and self._same_pages(buf.layout)
+                    and buf.device == self.device):
+                return self._update_from_pages(buf, h.gbuf, layer, hyper, st)
         with torch.cuda.stream(st):
             g = D.to_device_flat(grad, self.device)
         n = self.layout.numels[layer]
         if g.numel() != n:
             raise ProtocolError(f"gradient has {g.numel()} elements, layer {layer} has {n}")
         eng = self._eng
+        flag = eng.scratch(st).flag
         with torch.cuda.stream(st):
-            eng.flag.zero_()
+            flag.zero_()
         cc = D.contiguous_chunks_cached(n)
         D.check(N.lib().hm_reduce_stats(D.ptr(g), D.DT_OF_TORCH[g.dtype], D.ptr(eng.desc.static(cc)),
-                                         len(cc), D.ptr(eng.flag), None, None, D.sptr(st)))
+                                         len(cc), D.ptr(flag), None, None, D.sptr(st)))
         bc, bc_len = self._bias(hyper, [layer])
-        adam_launch(eng, self.layout.adam_chunks([layer], "tensor"), _group_rows([(0, 0, layer, 0)]),
-                    g, D.DT_OF_TORCH[g.dtype], self.p32_pool, self.m32_pool, self.v32_pool, None, 0,
-                    hyper, bc, bc_len, 0, self._steps, self._applied, eng.flag, None, True, st)
         with torch.cuda.stream(st):
-            return bool(self._applied[layer].item())
+            out = torch.empty(1, dtype=torch.int32, device=self.device)
+        adam_launch(eng, self.layout.adam_chunks([layer], "tensor"), _group_rows([(0, 0, 0, 0)]),
+                    g, D.DT_OF_TORCH[g.dtype], self.p32_pool, self.m32_pool, self.v32_pool, None, 0,
+                    hyper, bc, bc_len, 0, D.ptr(self._steps) + 4 * layer, out, flag, None, True, st)
+        return self._applied_result(out, st)
+
+    def _update_from_pages(self, buf, gbuf: int, layer: int, hyper, st):
+        L, span = buf.num_layers, buf.layout.elems16
+        nxt = buf._psel[layer] ^ 1
+        fidx = gbuf * L + layer
+        bc, bc_len = self._bias(hyper, [layer])
+        with torch.cuda.stream(st):
+            out = torch.empty(1, dtype=torch.int32, device=self.device)
+        # group 0 of the launch = this layer: steps[] is addressed at the
+        # layer's counter, applied[] is the per-call result word
+        adam_launch(self._eng, self.layout.adam_chunks([layer], "pool"),
+                    _group_rows([(gbuf * span, nxt * span, 0, fidx)]), buf.g16_pool, buf._dt,
+                    self.p32_pool, self.m32_pool, self.v32_pool, buf.p16_pool, buf._dt, hyper, bc, bc_len,
+                    0, D.ptr(self._steps) + 4 * layer, out, buf._flags, buf._sumsq, True, st)
+        buf._dirty.discard(fidx)
+        token = object()
+        buf._prepub[layer] = (token, nxt)
+        self._prepub[layer] = (weakref.ref(buf), token)
+        return self._applied_result(out, st)
+
+    def _applied_result(self, out: torch.Tensor, st):
+        if self._numpy:
+            with torch.cuda.stream(st):
+                return bool(out.item())
+        return Applied(out, st)
 
 
 # ---- ParamBuffer (hiermem/lockfree.py:174-263) ---------------------------------------
+
+_RING_ROWS = 1024
+
 
 class ParamBuffer(_Paged):
     """16-bit parameter/gradient page buffers owned by the buffering actor.
@@ -419,10 +608,16 @@ class ParamBuffer(_Paged):
     (lockfree.py:239) with zero clearing traffic.  Parameters: two page
     buffers per layer; a publish writes the inactive one and flips, and the
     (version, buffer, applied_iter) record swap keeps readers on the same
-    stream tear-free (lockfree.py:258-262)."""
+    stream tear-free (lockfree.py:258-262).
+
+    Per gradient slot (buffer x layer) the producers keep three fused
+    statistics next to the pages: the non-finite flag (the whole-layer
+    reject), the squared norm (clipping) and the ledger's running f64 sum.
+    ``ledger=False`` drops the ledger sums from the accumulate kernel (counts
+    are still kept)."""
 
     def __init__(self, initial_params, *, dtype: str = "fp16", page_bytes: int = PAGE_BYTES_DEFAULT,
-                 device=None, layout: PageLayout | None = None, ledger: bool = False,
+                 device=None, layout: PageLayout | None = None, ledger: bool = True,
                  world_size: int = 1, rank: int = 0, pool_alloc=None):
         if dtype not in D.TORCH16:
             raise ConfigError(f"dtype must be one of {sorted(D.TORCH16)}, got {dtype!r}")
@@ -443,20 +638,72 @@ class ParamBuffer(_Paged):
                 self.p16_pool.zero_()
             self._flags = torch.zeros(2 * L, dtype=torch.int32, device=self.device)
             self._sumsq = torch.zeros(2 * L, dtype=torch.float64, device=self.device)
+            self._lsum = torch.zeros(2 * L, dtype=torch.float64, device=self.device) if ledger else None
+            self._ring = torch.zeros(_RING_ROWS, 2 * L, dtype=torch.float64, device=self.device) \
+                if ledger else None
+        self._ring_pos = 0
         self._gsel = [0] * L
         self._psel = [0] * L
         self._pending = [0] * L
         self._max_iter = [-1] * L
         self._version = [0] * L
         self._applied_iter = [-1] * L
+        self._prepub = [None] * L          # (token, buffer) of p16 pre-published by update_layer
+        self._dirty: set[int] = set()      # slots handed over with their flag/norm not consumed
         self._ledger_on = ledger
         self.ledger = ConservationLedger(L)
+        if ledger:
+            self.ledger._resolver = self._ledger_flush
         for l, p in enumerate(initial_params):
             with torch.cuda.stream(st):
                 src = D.to_device_flat(p, self.device)
                 if src.dtype != torch.float32:
                     src = src.float()
             self._cast(src, N.DT_F32, self.p16_pool[0], self._dt, lay.seg_chunks(l, "16"), st)
+
+    # -- ledger ring ------------------------------------------------------------
+    def _ledger_row(self) -> tuple[int, int]:
+        """(row, device address) of a fresh ledger row (2L doubles, zeroed)."""
+        if self._ring_pos == _RING_ROWS:
+            self._ledger_flush()
+        r = self._ring_pos
+        self._ring_pos += 1
+        return r, D.ptr(self._ring) + r * self._ring.shape[1] * 8
+
+    def _ledger_flush(self) -> None:
+        """Resolve every pending ledger entry from the device rows (one
+        synchronisation), then recycle the rows."""
+        if not self._ring_pos:
+            return
+        torch.cuda.synchronize(self.device)
+        host = self._ring[:self._ring_pos].cpu().numpy()
+        self.ledger._resolve(host)
+        self._ring[:self._ring_pos].zero_()
+        torch.cuda.synchronize(self.device)   # rows are zero before any stream reuses them
+        self._ring_pos = 0
+
+    def _slots_table(self, slots) -> torch.Tensor:
+        return self._eng.desc.table(np.asarray(slots, dtype=np.uint32))
+
+    def _reset_dirty(self, slots, stream) -> None:
+        """Reset the flag / norm / ledger sum of slots about to take a first
+        message, if a hand-over left them unconsumed (one launch)."""
+        hit = [f for f in slots if f in self._dirty]
+        if not hit:
+            return
+        D.check(N.lib().hm_stats_take(D.ptr(self._eng.desc.table(np.asarray(hit, np.uint32), stream)),
+                                      len(hit), D.ptr(self._flags), D.ptr(self._sumsq),
+                                      D.ptr(self._lsum), None, D.sptr(stream)))
+        self._dirty.difference_update(hit)
+
+    def _record_consumed(self, layers, row: int) -> None:
+        """The take of ``layers`` wrote (sum, flag) pairs to ledger row ``row``."""
+        for i, l in enumerate(layers):
+            self.ledger._pend(self.ledger._consumed[l], row, 2 * i)
+
+    def _record_applies(self, layers, row: int) -> None:
+        for i, l in enumerate(layers):
+            self.ledger._apply_pending.append((l, row, 2 * i, 2 * i + 1))
 
     # -- reads ------------------------------------------------------------------
     def read(self, layer: int):
@@ -511,20 +758,54 @@ class ParamBuffer(_Paged):
         self._cast(pool, self._dt, out, self._dt, self.layout.seg_chunks(layer, "16", reverse=True), st)
         return out if raw else self._out(out, layer, readonly)
 
-    def _pool_sum(self, buf, layer, stream) -> float:
-        """f64 sum of the layer's gradient pages — ConservationLedger only
-        (check-only bookkeeping, never on the update path).  The pages are
-        unpacked by the page kernel and summed with torch's fixed-order
-        reduction so that the same data always yields the same float (the
-        ledger compares sums for equality, lockfree.py:311)."""
-        g = self._unpack16(self.g16_pool[buf], layer, stream=stream, raw=True)
-        with torch.cuda.stream(stream):
-            return float(g.double().sum().item())
-
     # -- writes -----------------------------------------------------------------
+    def _k3(self, src, src_dt, chunks, modes, slots, layers, stream, iteration) -> None:
+        """One accumulate launch (K3) + the host bookkeeping of its messages."""
+        self._reset_dirty([f for f, m in zip(slots, modes) if not m], stream)
+        row = None
+        if self._ledger_on:
+            row, rptr = self._ledger_row()
+        dmodes = None
+        if len(set(modes)) > 1:
+            m = np.zeros(2 * self.num_layers, dtype=np.uint8)
+            m[list(slots)] = modes
+            dmodes = self._eng.desc.table(m, stream)
+        D.check(N.lib().hm_accumulate(
+            D.ptr(src), src_dt, D.ptr(self.g16_pool), self._dt,
+            D.ptr(self._eng.desc.static(chunks)), len(chunks), modes[0] if dmodes is None else 0,
+            D.ptr(dmodes), D.ptr(self._flags), D.ptr(self._sumsq),
+            D.ptr(self._lsum) if self._ledger_on else None, rptr if self._ledger_on else None,
+            None, D.sptr(stream)))
+        for l, f in zip(layers, slots):
+            if row is not None:
+                self.ledger._pend(self.ledger._produced[l], row, f)
+            self.ledger.messages_accumulated[l] += 1
+            self._pending[l] += 1
+            self._max_iter[l] = max(self._max_iter[l], iteration)
+
+    def _acc_plan(self, layers, base_of) -> np.ndarray:
+        """hm_seg_chunk plan accumulating a flat source into the CURRENT
+        gradient buffers of ``layers`` (cached per buffer selection)."""
+        L, lay = self.num_layers, self.layout
+        sel = tuple(self._gsel[l] for l in layers)
+        cache = self.__dict__.setdefault("_acc_plans", {})
+        key = (tuple(layers), sel, base_of is None)
+        if key not in cache:
+            parts = []
+            for l, b in zip(layers, sel):
+                c = lay.seg_chunks(l, "16").copy()
+                if base_of is not None:
+                    c["src_off"] += base_of(l)
+                c["dst_off"] += b * lay.elems16
+                c["slot"] = b * L + l
+                parts.append(c)
+            cache[key] = np.concatenate(parts)
+        return cache[key]
+
     def accumulate(self, msg: GradMessage, *, stream=None) -> None:
         """g16 = rn16(f32(g16) + f32(payload)) over the layer's pages, with the
-        layer's non-finite flag and squared norm fused in (lockfree.py:210-224)."""
+        layer's non-finite flag, squared norm and ledger sum fused in
+        (lockfree.py:210-224)."""
         layer = msg.layer
         if not (0 <= layer < self.num_layers):
             raise ProtocolError(f"gradient for unknown layer {layer}")
@@ -534,31 +815,14 @@ class ParamBuffer(_Paged):
         st = self._stream(stream)
         with torch.cuda.stream(st):
             src = D.to_device_flat(msg.payload, self.device)
-        buf = self._gsel[layer]
-        add = self._pending[layer] > 0
-        old = self._pool_sum(buf, layer, st) if (self._ledger_on and add) else 0.0
-        if not add:  # first message into this buffer: reset its flag and norm
-            with torch.cuda.stream(st):
-                self._flags[buf * self.num_layers + layer] = 0
-                self._sumsq[buf * self.num_layers + layer] = 0
-        ch = self.layout.seg_chunks(layer, "16")
-        fidx = buf * self.num_layers + layer
-        D.check(N.lib().hm_accumulate(
-            D.ptr(src), D.DT_OF_TORCH[src.dtype], D.ptr(self.g16_pool[buf]), self._dt,
-            D.ptr(self._eng.desc.static(ch)), len(ch), 1 if add else 0, None,
-            D.ptr(self._flags) + 4 * fidx, D.ptr(self._sumsq) + 8 * fidx, D.sptr(st)))
-        if self._ledger_on:
-            self.ledger.record_accumulate(layer, self._pool_sum(buf, layer, st) - old)
-        else:
-            self.ledger.messages_accumulated[layer] += 1
-        self._pending[layer] += 1
-        self._max_iter[layer] = max(self._max_iter[layer], msg.iteration)
+        f = self._gsel[layer] * self.num_layers + layer
+        self._k3(src, D.DT_OF_TORCH[src.dtype], self._acc_plan([layer], None),
+                 [1 if self._pending[layer] > 0 else 0], [f], [layer], st, msg.iteration)
 
     def accumulate_flat(self, flat, iteration: int, *, stream=None) -> None:
         """Accumulate one flat gradient covering every layer in order (the
-        layout a backward pass writes) with ONE K3 launch: the same arithmetic
-        and flags as one ``accumulate`` per layer.  Ledger sums need per-layer
-        reductions, so a ledger-enabled buffer falls back to per-layer calls."""
+        layout a backward pass writes) with ONE K3 launch: the same arithmetic,
+        flags and ledger entries as one ``accumulate`` per layer."""
         L, lay = self.num_layers, self.layout
         st = self._stream(stream)
         with torch.cuda.stream(st):
@@ -566,64 +830,30 @@ class ParamBuffer(_Paged):
         if src.numel() != sum(lay.numels):
             raise ProtocolError(f"flat gradient has {src.numel()} elements, layers hold "
                                 f"{sum(lay.numels)}")
-        if self._ledger_on:
-            pos = 0
-            for l, n in enumerate(lay.numels):
-                self.accumulate(GradMessage(l, src[pos:pos + n].view(self._shapes[l]), iteration),
-                                stream=st)
-                pos += n
-            return
-        key = tuple(self._gsel)
-        cache = self.__dict__.setdefault("_flat_cache", {})
-        if key not in cache:
-            parts, base = [], 0
-            for l, n in enumerate(lay.numels):
-                c = lay.seg_chunks(l, "16").copy()
-                c["src_off"] += base
-                c["dst_off"] += key[l] * lay.elems16
-                c["slot"] = key[l] * L + l
-                parts.append(c)
-                base += n
-            cache[key] = np.concatenate(parts)
-        chunks = cache[key]
-        modes = np.zeros(2 * L, dtype=np.uint8)
-        reset = []
-        for l in range(L):
-            f = self._gsel[l] * L + l
-            if self._pending[l] > 0:
-                modes[f] = 1
-            else:
-                reset.append(f)
-        with torch.cuda.stream(st):
-            if reset:
-                if reset == list(range(reset[0], reset[0] + len(reset))):
-                    self._flags[reset[0]:reset[0] + len(reset)].zero_()
-                    self._sumsq[reset[0]:reset[0] + len(reset)].zero_()
-                else:
-                    idx = torch.tensor(reset, dtype=torch.int64, device=self.device)
-                    self._flags.index_fill_(0, idx, 0)
-                    self._sumsq.index_fill_(0, idx, 0)
-        dmodes = self._eng.desc.table(modes)
-        D.check(N.lib().hm_accumulate(
-            D.ptr(src), D.DT_OF_TORCH[src.dtype], D.ptr(self.g16_pool), self._dt,
-            D.ptr(self._eng.desc.static(chunks)), len(chunks), 0, D.ptr(dmodes),
-            D.ptr(self._flags), D.ptr(self._sumsq), D.sptr(st)))
-        for l in range(L):
-            self.ledger.messages_accumulated[l] += 1
-            self._pending[l] += 1
-            self._max_iter[l] = max(self._max_iter[l], iteration)
+        starts = self.__dict__.setdefault("_starts", np.cumsum([0] + lay.numels[:-1]))
+        layers = list(range(L))
+        self._k3(src, D.DT_OF_TORCH[src.dtype], self._acc_plan(layers, lambda l: int(starts[l])),
+                 [1 if self._pending[l] > 0 else 0 for l in layers],
+                 [self._gsel[l] * L + l for l in layers], layers, st, iteration)
 
-    def _hand_over(self, layer: int, stream):
-        """Clear-at-take bookkeeping shared by take() and sweep()."""
+    def _hand_over(self, layer: int):
+        """Clear-at-take bookkeeping shared by every update path: the active
+        gradient buffer is handed over and accumulation flips to the other."""
         buf = self._gsel[layer]
         count, newest = self._pending[layer], self._max_iter[layer]
-        if self._ledger_on:
-            self.ledger.record_take(layer, self._pool_sum(buf, layer, stream), count)
-        else:
-            self.ledger.messages_consumed[layer] += count
+        self.ledger.messages_consumed[layer] += count
         self._gsel[layer] = buf ^ 1
         self._pending[layer] = 0
         return buf, count, newest
+
+    def _published(self, layer: int, applied_iter=None) -> int:
+        """Flip the record to the inactive buffer just written (lockfree.py:258-262)."""
+        self._psel[layer] ^= 1
+        self._version[layer] += 1
+        self._prepub[layer] = None
+        if applied_iter is not None:
+            self._applied_iter[layer] = applied_iter
+        return self._version[layer]
 
     def take(self, layer: int, *, stream=None):
         """Atomically hand over and clear the accumulated gradient: returns
@@ -632,16 +862,24 @@ class ParamBuffer(_Paged):
         if self._pending[layer] == 0:
             return None
         st = self._stream(stream)
-        buf, count, newest = self._hand_over(layer, st)
+        buf, count, newest = self._hand_over(layer)
         with torch.cuda.stream(st):
             g = torch.empty(self.layout.numels[layer], dtype=torch.float32, device=self.device)
         self._cast(self.g16_pool[buf], self._dt, g, N.DT_F32,
                    self.layout.seg_chunks(layer, "16", reverse=True), st)
         fidx = buf * self.num_layers + layer
-        with torch.cuda.stream(st):
-            self._flags[fidx] = 0
-            self._sumsq[fidx] = 0
-        return self._out(g, layer), count, newest
+        if self._ledger_on:   # record_take: snapshot + reset the running sum
+            row, rptr = self._ledger_row()
+            D.check(N.lib().hm_stats_take(D.ptr(self._eng.desc.table(np.array([fidx], np.uint32), st)), 1,
+                                          None, None, D.ptr(self._lsum), rptr, D.sptr(st)))
+            self._record_consumed([layer], row)
+        # the reject flag and norm stay for an update_layer of this tensor;
+        # otherwise they are reset before the slot's next first message
+        self._dirty.add(fidx)
+        out = self._out(g, layer)
+        if isinstance(out, torch.Tensor):
+            out._hm_taken = _Taken(self, layer, buf, out._version)
+        return out, count, newest
 
     def publish(self, layer: int, p32, applied_iter: int | None = None, clear: bool = True,
                 *, stream=None) -> int:
@@ -650,12 +888,26 @@ class ParamBuffer(_Paged):
         self._check_layer(layer)
         st = self._stream(stream)
         if clear:
-            if self._ledger_on:
-                total = self._pool_sum(self._gsel[layer], layer, st) if self._pending[layer] else 0.0
-                self.ledger.record_take(layer, total, self._pending[layer])
-            else:
+            if self._pending[layer]:
+                fidx = self._gsel[layer] * self.num_layers + layer
+                row = rptr = None
+                if self._ledger_on:
+                    row, rptr = self._ledger_row()
+                D.check(N.lib().hm_stats_take(D.ptr(self._eng.desc.table(np.array([fidx], np.uint32), st)),
+                                              1, D.ptr(self._flags), D.ptr(self._sumsq),
+                                              D.ptr(self._lsum), rptr, D.sptr(st)))
+                if row is not None:
+                    self._record_consumed([layer], row)
+                self._dirty.discard(fidx)
                 self.ledger.messages_consumed[layer] += self._pending[layer]
+            elif self._ledger_on:
+                self.ledger._consumed[layer].append(0.0)
             self._pending[layer] = 0
+        tag = getattr(p32, "_hm_prepub", None) if isinstance(p32, torch.Tensor) else None
+        pre = self._prepub[layer]
+        if (tag is not None and pre is not None and tag[0]() is self and tag[1] is pre[0]
+                and tag[2] == layer and p32._version == tag[3] and pre[1] == self._psel[layer] ^ 1):
+            return self._published(layer, applied_iter)   # update_layer already cast these values
         with torch.cuda.stream(st):
             src = D.to_device_flat(p32, self.device)
             if src.dtype != torch.float32:
@@ -665,11 +917,7 @@ class ParamBuffer(_Paged):
                                 f"{self.layout.numels[layer]}")
         nxt = self._psel[layer] ^ 1
         self._cast(src, N.DT_F32, self.p16_pool[nxt], self._dt, self.layout.seg_chunks(layer, "16"), st)
-        self._psel[layer] = nxt
-        self._version[layer] += 1
-        if applied_iter is not None:
-            self._applied_iter[layer] = applied_iter
-        return self._version[layer]
+        return self._published(layer, applied_iter)
 
 
 def publish_params(buffer: ParamBuffer, layer: int, p32) -> None:
@@ -697,14 +945,84 @@ class SweepResult:
         return {l: bool(a[l]) for l in self.layers}
 
 
+class UpdateTicket:
+    """One update of a set of layers over a ParamBuffer, shared by every
+    update path (fused sweep, pinned-host / SSD swap sweeps, DP steps): the
+    hand-over (take), the prologue's group rows, the ledger row that records
+    what was consumed and applied, and the publish flip at the end."""
+
+    def __init__(self, buffer: ParamBuffer, layers, flag_of=None):
+        self.buffer = buffer
+        self.layers = list(layers)
+        L, span = buffer.num_layers, buffer.layout.elems16
+        rows, self.counts, self.newest = [], [], []
+        for l in self.layers:
+            gbuf, count, new = buffer._hand_over(l)
+            rows.append((gbuf * span, (buffer._psel[l] ^ 1) * span, l,
+                         gbuf * L + l if flag_of is None else flag_of(l)))
+            self.counts.append(count)
+            self.newest.append(new)
+        self.groups = _group_rows(rows)
+        self.row = None
+        self.ledger_out = 0
+        if buffer._ledger_on:
+            self.row, self.ledger_out = buffer._ledger_row()
+
+    def lsum(self, base_slot: int = 0) -> int:
+        """Address of the ledger running sums as the prologue indexes them
+        (``base_slot`` shifts it when the prologue's flags are not the buffer's)."""
+        b = self.buffer
+        return D.ptr(b._lsum) + 8 * base_slot if b._ledger_on else 0
+
+    def finish(self, consumed_flags: bool = True) -> None:
+        """Record the ledger entries and flip every layer's published record.
+        ``consumed_flags=False``: the prologue consumed other flags (DP steps),
+        so the buffer's own slots are reset before their next first message."""
+        b = self.buffer
+        L = b.num_layers
+        for l, new in zip(self.layers, self.newest):
+            b._published(l, new)
+        slots = [int(r["flag"]) for r in self.groups]
+        if consumed_flags:
+            b._dirty.difference_update(slots)
+        else:
+            b._dirty.update(int(r["g_shift"]) // b.layout.elems16 * L + l
+                            for r, l in zip(self.groups, self.layers))
+        if self.row is not None:
+            b._record_consumed(self.layers, self.row)
+            b._record_applies(self.layers, self.row)
+
+
+def update_prologue(ticket: UpdateTicket, masters, hyper, stream, *, flags=None, sumsq=None,
+                    lsum: int | None = None):
+    """The ticket's prologue (reject / step / bias lookup, ledger record) for
+    callers that run the main pass themselves (swap tiers, DP steps).
+    ``flags`` / ``sumsq`` default to the buffer's own fused statistics.
+    Returns (device group table, rt scratch, hyper struct) for the main pass,
+    which must run on ``stream`` (the rt scratch is the stream's)."""
+    b = ticket.buffer
+    eng = masters._eng
+    dgroups = eng.desc.table(ticket.groups, stream)
+    rt = eng.rt_scratch(len(ticket.groups), stream)
+    bc, bc_len = masters._bias(hyper, ticket.layers)
+    hc = D.hyper_c(hyper)
+    D.check(N.lib().hm_adam_prologue(
+        D.ptr(dgroups), len(ticket.groups), D.ptr(rt), hc, D.ptr(bc), bc_len, 0, D.ptr(masters._steps),
+        D.ptr(masters._applied), D.addr(b._flags if flags is None else flags),
+        D.addr(b._sumsq if sumsq is None else sumsq), 1, (ticket.lsum() if lsum is None else lsum) or None,
+        ticket.ledger_out or None, D.sptr(stream)))
+    return dgroups, rt, hc
+
+
 def sweep(buffer: ParamBuffer, masters: MasterState, hyper: AdamHyper, layers=None, *,
-          stream=None, record_ledger: bool = True) -> SweepResult:
+          stream=None, opts=None) -> SweepResult:
     """The updating actor's per-layer loop body (hiermem/lockfree.py:624-639):
     for every layer with pending gradients, take (clear) -> update_layer ->
     publish(clear=False, applied_iter=newest), fused into ONE prologue and
     ONE page-Adam launch over all their page segments: reads g16 + p/m/v
     (14 B/param), writes p/m/v + p16 (14 B/param).  Asynchronous; the
-    whole-layer reject and step rollback happen on the device."""
+    whole-layer reject and step rollback happen on the device.  With
+    ``hyper.max_norm > 0`` the clip norm is that of the swept layers."""
     lay = buffer.layout
     if masters.layout.numels != lay.numels or masters.layout.page_bytes != lay.page_bytes \
             or masters.layout.world_size != lay.world_size:
@@ -714,28 +1032,16 @@ def sweep(buffer: ParamBuffer, masters: MasterState, hyper: AdamHyper, layers=No
     sel = [l for l in order if buffer._pending[l] > 0]
     if not sel:
         return SweepResult(masters, [], [], [])
-    L, span = buffer.num_layers, lay.elems16
-    rows, counts, newest = [], [], []
-    for l in sel:
-        gbuf, count, new = buffer._hand_over(l, st)
-        rows.append((gbuf * span, (buffer._psel[l] ^ 1) * span, l, gbuf * L + l))
-        counts.append(count)
-        newest.append(new)
+    t = UpdateTicket(buffer, sel)
     bc, bc_len = masters._bias(hyper, sel)
-    adam_launch(masters._eng, lay.adam_chunks(sel, "pool"), _group_rows(rows),
+    for l in sel:
+        masters._prepub[l] = None
+    adam_launch(masters._eng, lay.adam_chunks(sel, "pool"), t.groups,
                 buffer.g16_pool, buffer._dt, masters.p32_pool, masters.m32_pool, masters.v32_pool,
                 buffer.p16_pool, buffer._dt, hyper, bc, bc_len, 0, masters._steps, masters._applied,
-                buffer._flags, buffer._sumsq, True, st)
-    for l, new in zip(sel, newest):
-        buffer._psel[l] ^= 1
-        buffer._version[l] += 1
-        buffer._applied_iter[l] = new
-    if buffer._ledger_on and record_ledger:
-        with torch.cuda.stream(st):
-            ok = masters._applied.cpu().tolist()
-        for l in sel:
-            buffer.ledger.record_apply(l, buffer.ledger.consumed_sums[l][-1], rejected=not ok[l])
-    return SweepResult(masters, sel, counts, newest)
+                buffer._flags, buffer._sumsq, True, st, lsum=t.lsum(), ledger_out=t.ledger_out, opts=opts)
+    t.finish()
+    return SweepResult(masters, sel, t.counts, t.newest)
 
 
 class _MultiResult(SweepResult):
@@ -792,59 +1098,86 @@ def ingest(buffer: ParamBuffer, host_grad, iteration: int = 0, *, groups: int = 
             landed = torch.cuda.Event()
             landed.record(cs)
         st.wait_event(landed)
-        gkey = ("acc", tuple(grp), tuple(buffer._gsel[l] for l in grp))
-        if gkey not in cache:
-            rows = []
-            for l in grp:
-                c = lay.seg_chunks(l, "16").copy()
-                c["src_off"] += int(starts[l])
-                c["dst_off"] += buffer._gsel[l] * lay.elems16
-                c["slot"] = buffer._gsel[l] * L + l
-                rows.append(c)
-            cache[gkey] = np.concatenate(rows)
-        chunks = cache[gkey]
-        modes = np.zeros(2 * L, dtype=np.uint8)
-        reset = []
-        for l in grp:
-            f = buffer._gsel[l] * L + l
-            if buffer._pending[l] > 0:
-                modes[f] = 1
-            else:
-                reset.append(f)
-        if reset:
-            idx = buffer._eng.desc.table(np.array(reset, dtype=np.int64)).view(torch.int64)
-            with torch.cuda.stream(st):
-                buffer._flags.index_fill_(0, idx, 0)
-                buffer._sumsq.index_fill_(0, idx, 0)
-        D.check(N.lib().hm_accumulate(
-            D.ptr(staging), buffer._dt, D.ptr(buffer.g16_pool), buffer._dt,
-            D.ptr(buffer._eng.desc.static(chunks)), len(chunks), 0,
-            D.ptr(buffer._eng.desc.table(modes)), D.ptr(buffer._flags), D.ptr(buffer._sumsq),
-            D.sptr(st)))
+        buffer._k3(staging, buffer._dt, buffer._acc_plan(grp, lambda l: int(starts[l])),
+                   [1 if buffer._pending[l] > 0 else 0 for l in grp],
+                   [buffer._gsel[l] * L + l for l in grp], grp, st, iteration)
         ev = torch.cuda.Event()
         ev.record(st)
         done.append(ev)
-        for l in grp:
-            buffer.ledger.messages_accumulated[l] += 1
-            buffer._pending[l] += 1
-            buffer._max_iter[l] = max(buffer._max_iter[l], iteration)
         if after_group is not None:
             after_group(grp)
     return done
 
 
 def ingest_sweep(buffer: ParamBuffer, masters: MasterState, host_grad, hyper: AdamHyper,
-                 iteration: int = 0, *, groups: int = 8, stream=None, copy_stream=None) -> SweepResult:
+                 iteration: int = 0, *, groups: int = 8, stream=None, copy_stream=None,
+                 results_to=None) -> SweepResult:
     """One update step fed by a flat gradient in (pinned) host memory — what a
     host-side producer hands the updating actor.  Per contiguous layer group:
     cudaMemcpyAsync of the group's slice on a copy stream -> K3 accumulate
     into its pages when it lands -> fused sweep of the group, so the PCIe
     transfer of group k+1 overlaps the update of group k and the step costs
     about one transfer of the gradient (the reference's fetch/offload are
-    DelayModel sleeps, hiermem/lockfree.py:90-94, 562-569)."""
+    DelayModel sleeps, hiermem/lockfree.py:90-94, 562-569).
+
+    ``results_to`` (a pinned host 16-bit tensor of every layer's elements in
+    layer order): each group's freshly published parameters are copied back
+    to the host on a second copy stream right after the group's update, so
+    the D2H of group k overlaps the H2D of group k+1 (PCIe is full duplex) —
+    the step returns its result, not just the applied flags.
+
+    Global grad-norm clipping needs every group's norm before the first
+    update, so it is refused here (use accumulate + ``sweep``)."""
+    if getattr(hyper, "max_norm", 0.0) > 0:
+        raise ConfigError("ingest_sweep updates group by group: global grad-norm clipping "
+                          "(max_norm > 0) needs the whole gradient first; use accumulate_flat + sweep")
     st = buffer._stream(stream)
     parts = []
+    d2h = None
+    if results_to is not None:
+        lay = buffer.layout
+        if results_to.dtype != buffer._t16 or results_to.numel() != sum(lay.numels):
+            raise ProtocolError(f"results_to must be {buffer._t16} with {sum(lay.numels)} elements")
+        cache = buffer.__dict__.setdefault("_ingest", {})
+        d2h = cache.setdefault("d2h", torch.cuda.Stream(buffer.device))
+        starts = cache.setdefault("starts", np.cumsum([0] + lay.numels[:-1]))
+
+    def after(grp):
+        parts.append(sweep(buffer, masters, hyper, layers=list(reversed(grp)), stream=st))
+        if d2h is not None:
+            _publish_to_host(buffer, grp, results_to, starts, st, d2h)
+
     ingest(buffer, host_grad, iteration, groups=groups, stream=st, copy_stream=copy_stream,
-           after_group=lambda grp: parts.append(
-               sweep(buffer, masters, hyper, layers=list(reversed(grp)), stream=st)))
+           after_group=after)
+    if d2h is not None:
+        st.wait_stream(d2h)
     return _MultiResult(masters, parts)
+
+
+def _publish_to_host(buffer: ParamBuffer, grp, host, starts, st, d2h) -> None:
+    """D2H of the published pages of layer group ``grp`` into the flat host
+    tensor: one cudaMemcpyAsync per contiguous run of the pool (layers
+    allocated in order are one run), queued on ``d2h`` behind the group's
+    update on ``st``."""
+    lay = buffer.layout
+    cache = buffer.__dict__.setdefault("_d2h_runs", {})
+    key = (tuple(grp), tuple(buffer._psel[l] for l in grp))
+    if key not in cache:
+        runs = []
+        E, esz = lay.E, 2
+        for l in grp:
+            base = int(starts[l])
+            for s in lay.segments[l]:
+                src = (buffer._psel[l] * lay.elems16 + lay.slot16(s.page) * E + s.off) * esz
+                dst = (base + s.pos) * esz
+                if runs and runs[-1][0] + runs[-1][2] == src and runs[-1][1] + runs[-1][2] == dst:
+                    runs[-1][2] += s.n * esz
+                else:
+                    runs.append([src, dst, s.n * esz])
+        cache[key] = np.array([tuple(r) for r in runs], dtype=N.COPY_DESC)
+    runs = cache[key]
+    ev = torch.cuda.Event()
+    ev.record(st)
+    d2h.wait_event(ev)
+    D.check(N.lib().hm_memcpy_runs(D.ptr(buffer.p16_pool), D.ptr(host), runs.ctypes.data, len(runs), 2,
+                                   D.sptr(d2h)))

@@ -163,7 +163,7 @@ class DevicePageManager(PageManager):
                 with torch.cuda.stream(st):
                     dev = raw.to(self.device, non_blocking=raw.is_pinned()) if not raw.is_cuda else raw
                 d = _descs(rows)
-                D.check(lib.hm_copy_runs(D.ptr(dev), D.ptr(store), D.ptr(self._up(d)), len(d), D.sptr(st)))
+                D.check(lib.hm_copy_runs(D.ptr(dev), D.ptr(store), D.ptr(self._up(d, st)), len(d), D.sptr(st)))
                 if dev is not raw:
                     dev.record_stream(st)
             elif tier is Tier.SSD:
@@ -194,7 +194,7 @@ class DevicePageManager(PageManager):
             inv = [(dpos, s, n) for s, dpos, n in rows]
             if tier is Tier.GPU:
                 d = _descs(inv)
-                D.check(lib.hm_copy_runs(D.ptr(store), D.ptr(out), D.ptr(self._up(d)), len(d), D.sptr(st)))
+                D.check(lib.hm_copy_runs(D.ptr(store), D.ptr(out), D.ptr(self._up(d, st)), len(d), D.sptr(st)))
             elif tier is Tier.SSD:
                 for src, dst, n in inv:
                     chunk = torch.from_numpy(self._ssd_read_bytes(src, n))
@@ -206,9 +206,14 @@ class DevicePageManager(PageManager):
         dt = torch.float32 if t.dtype == "fp32" else torch.float16
         return out.view(dt)
 
-    def _up(self, d: np.ndarray) -> torch.Tensor:
-        return torch.from_numpy(d.view(np.uint8).copy()).to(self.device) if len(d) else \
-            torch.empty(8, dtype=torch.uint8, device=self.device)
+    def _up(self, d: np.ndarray, stream=None) -> torch.Tensor:
+        """Upload copy descriptors for a launch on ``stream``: allocated and
+        copied on that stream, so the block cannot be handed to another
+        upload before the kernel that reads it has run."""
+        st = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            return torch.from_numpy(d.view(np.uint8).copy()).to(self.device) if len(d) else \
+                torch.empty(8, dtype=torch.uint8, device=self.device)
 
     # -- movement with data -----------------------------------------------------------
     def _tier_of(self, pid: int) -> Tier:
@@ -288,8 +293,8 @@ class DevicePageManager(PageManager):
                 scatter.append((pos, a1, n))
                 pos += n
             g, s = _descs(gather), _descs(scatter)
-            D.check(N.lib().hm_copy_runs(D.ptr(store), D.ptr(tmp), D.ptr(self._up(g)), len(g), D.sptr(st)))
-            D.check(N.lib().hm_copy_runs(D.ptr(tmp), D.ptr(store), D.ptr(self._up(s)), len(s), D.sptr(st)))
+            D.check(N.lib().hm_copy_runs(D.ptr(store), D.ptr(tmp), D.ptr(self._up(g, st)), len(g), D.sptr(st)))
+            D.check(N.lib().hm_copy_runs(D.ptr(tmp), D.ptr(store), D.ptr(self._up(s, st)), len(s), D.sptr(st)))
         elif tier is Tier.SSD:
             tmp = [self._ssd_read_bytes(a0, n) for a0, _, n in moves]   # gather first: chains
             for (a0, a1, n), buf in zip(moves, tmp):

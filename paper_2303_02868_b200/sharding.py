@@ -36,6 +36,7 @@ from . import _device as D
 from . import _native as N
 from .errors import ConfigError
 from .layout import PageLayout
+from .lockfree import UpdateTicket, update_prologue
 
 
 @dataclass(frozen=True)
@@ -176,25 +177,10 @@ class ShardedPageStep:
             if getattr(hyper, "max_norm", 0.0) > 0:
                 dist.all_reduce(self.sumsq, op=dist.ReduceOp.SUM, group=self.group)
             mark("check")
-        counts, newest = [], []
-        for l in range(L):
-            _, c, n = buf._hand_over(l, st)
-            counts.append(c)
-            newest.append(n)
-        span = lay.elems16
-        rows = [(gsel * span, (buf._psel[l] ^ 1) * span, l, l) for l in range(L)]
-        groups = np.zeros(L, dtype=N.GROUP_LAUNCH)
-        for i, r in enumerate(rows):
-            groups[i] = r
-        eng = ms._eng
-        dgroups = eng.desc.table(groups)
-        rt = eng.rt_scratch(L)
-        bc, bc_len = ms._bias(hyper, range(L))
-        hc = D.hyper_c(hyper)
-        lib = N.lib()
-        D.check(lib.hm_adam_prologue(D.ptr(dgroups), L, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
-                                     D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(self.flags),
-                                     D.ptr(self.sumsq), 1, D.sptr(st)))
+        t = UpdateTicket(buf, range(L), flag_of=lambda l: l)
+        dgroups, rt, hc = update_prologue(t, ms, hyper, st, flags=self.flags, sumsq=self.sumsq,
+                                          lsum=t.lsum(gsel * L))
+        eng, lib = ms._eng, N.lib()
         new_p = (buf._psel[0] ^ 1)
         ppool = buf.p16_pool[new_p]
         works = []
@@ -203,7 +189,7 @@ class ShardedPageStep:
             D.check(lib.hm_adam_main(D.ptr(eng.desc.static(chunks)), len(chunks), D.ptr(dgroups),
                                      D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
                                      D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), D.ptr(buf.p16_pool),
-                                     buf._dt, hc, D.sptr(st)))
+                                     buf._dt, hc, None, D.sptr(st)))
             done = torch.cuda.Event()
             done.record(st)
             self.comm.wait_event(done)
@@ -216,10 +202,7 @@ class ShardedPageStep:
         st.wait_stream(self.comm)
         with torch.cuda.stream(st):
             mark("ag")
-        for l in range(L):
-            buf._psel[l] ^= 1
-            buf._version[l] += 1
-            buf._applied_iter[l] = newest[l]
+        t.finish(consumed_flags=False)
         if timings is not None:
             timings["_marks"] = marks
         return list(range(L))
@@ -282,6 +265,8 @@ class FusedShardedPageStep:
         self.s_ptrs = [int(p) for p in self.h_s.buffer_ptrs]
         self._check_chunks = lay.pool_chunks(range(L), "16", owned_only=True)
         self._adam_chunks = lay.adam_chunks(range(L), "pool", owned_only=True)
+        # pinned-host / SSD state tier: the state is streamed in step()
+        self.host_tier = hasattr(masters, "stream_update")
 
     @staticmethod
     def _arr(ptrs):
@@ -328,7 +313,8 @@ class FusedShardedPageStep:
         return cache[groups]
 
     def step_pipelined(self, hyper, groups: int = 4, *, reduce_ctas: int = 0, update_ctas: int = 0,
-                       reduce_sms: int = 0, ready=None, stream=None,
+                       reduce_sms: int = 0, ready=None, stream=None, ag_publish: int = -1,
+                       reduce_wide: int = -1, reduce_width: int = -1,
                        timings: dict | None = None):
         """``step`` with the layers cut into contiguous groups and two streams:
         the reduce-scatter + check of group k+1 runs while group k is updated
@@ -347,8 +333,12 @@ class FusedShardedPageStep:
         run on every rank.  With NVLS the RS leg is outbound-heavy (S out, S/N
         in per GPU) and the AG leg inbound-heavy (S/N out, S in), so
         overlapping them moves (1 + 1/N)·S per link direction instead of
-        2·(N−1)/N·S."""
+        2·(N−1)/N·S.  Launch settings travel with each launch (hm_launch_opts),
+        nothing process-wide is changed."""
         buf, ms, lay = self.buffer, self.masters, self.layout
+        if self.host_tier:
+            raise ConfigError("the layer-group pipeline keeps the state in HBM; a host/SSD-tier "
+                              "DP step streams the state in step()")
         st = buf._stream(stream)
         L = buf.num_layers
         if any(p == 0 for p in buf._pending):
@@ -365,6 +355,8 @@ class FusedShardedPageStep:
         clip = getattr(hyper, "max_norm", 0.0) > 0
         if clip:
             raise ConfigError("global grad-norm clipping needs every group's norm first: use step()")
+        rs_opts = D.opts(grid_ctas=int(reduce_ctas), reduce_wide=reduce_wide, reduce_width=reduce_width)
+        up_opts = D.opts(grid_ctas=int(update_ctas), ag_publish=ag_publish)
         marks = {}
 
         def mark(name, s):
@@ -396,49 +388,43 @@ class FusedShardedPageStep:
                 self.flags_local.zero_()
         gp = self._arr([p + gsel * span_b for p in self.g_ptrs])
         mc = self.mc_g + gsel * span_b if self.mc_g else None
-        counts, newest = [0] * L, [0] * L
-        for l in range(L):
-            _, counts[l], newest[l] = buf._hand_over(l, st)
+        t = UpdateTicket(buf, range(L), flag_of=lambda l: l)
         bc, bc_len = ms._bias(hyper, range(L))
         hc = D.hyper_c(hyper)
         rts = self.__dict__.setdefault("_rts", {})
-        D.check(lib.hm_set_dp_reduce_ctas(int(reduce_ctas)))   # persistent reduce grid (0 = per chunk)
-        D.check(lib.hm_set_dp_update_ctas(int(update_ctas)))   # persistent update grid (0 = per chunk)
-        try:
-            for k, (grp, check, adam) in enumerate(plan):
-                first, n = grp[0], len(grp)
-                with torch.cuda.stream(rs):
-                    if ready is not None:
-                        rs.wait_event(ready[k])
-                        self.h_g.barrier(channel=0)                  # group k landed on every rank
-                    D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
-                                                   D.ptr(eng.desc.static(check)), len(check),
-                                                   D.ptr(self.flags_local), None, D.sptr(rs)))
-                    self.h_f.barrier(channel=1)                      # group k's flags visible everywhere
-                    done = torch.cuda.Event()
-                    done.record(rs)
-                up.wait_event(done)
-                with torch.cuda.stream(up):
-                    D.check(lib.hm_dp_flags_merge(self._arr([p + 4 * first for p in self.f_ptrs]), None,
-                                                  self.n, n, D.ptr(self.flags) + 4 * first, None, D.sptr(up)))
-                    rows = np.zeros(n, dtype=N.GROUP_LAUNCH)
-                    for i, l in enumerate(grp):
-                        rows[i] = (gsel * span, (psel ^ 1) * span, l, l)
-                    dgroups = eng.desc.table(rows)
-                    if (k, n) not in rts:
-                        rts[(k, n)] = torch.empty(n * N.GROUP_RT_BYTES, dtype=torch.uint8, device=self.device)
-                    rt = rts[(k, n)]
-                    D.check(lib.hm_adam_prologue(D.ptr(dgroups), n, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
-                                                 D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(self.flags),
-                                                 None, 1, D.sptr(up)))
-                    D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups),
-                                                D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
-                                                D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
-                                                self.n, self.mc_p if self.mc_p else None, buf._dt, hc,
-                                                D.sptr(up)))
-        finally:   # process-wide knobs: never leak a persistent grid into later launches
-            D.check(lib.hm_set_dp_reduce_ctas(0))
-            D.check(lib.hm_set_dp_update_ctas(0))
+        for k, (grp, check, adam) in enumerate(plan):
+            first, n = grp[0], len(grp)
+            with torch.cuda.stream(rs):
+                if ready is not None:
+                    rs.wait_event(ready[k])
+                    self.h_g.barrier(channel=0)                  # group k landed on every rank
+                D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
+                                               D.ptr(eng.desc.static(check)), len(check),
+                                               D.ptr(self.flags_local), None, rs_opts, D.sptr(rs)))
+                self.h_f.barrier(channel=1)                      # group k's flags visible everywhere
+                done = torch.cuda.Event()
+                done.record(rs)
+            up.wait_event(done)
+            with torch.cuda.stream(up):
+                D.check(lib.hm_dp_flags_merge(self._arr([p + 4 * first for p in self.f_ptrs]), None,
+                                              self.n, n, D.ptr(self.flags) + 4 * first, None, D.sptr(up)))
+                rows = t.groups[first:first + n].copy()
+                rows["flag"] -= first                            # the merged flags of this group start at 0
+                rows["group"] = grp
+                dgroups = eng.desc.table(rows, up)
+                if (k, n) not in rts:
+                    rts[(k, n)] = torch.empty(n * N.GROUP_RT_BYTES, dtype=torch.uint8, device=self.device)
+                rt = rts[(k, n)]
+                ledger_out = t.ledger_out + 16 * first if t.ledger_out else None
+                D.check(lib.hm_adam_prologue(D.ptr(dgroups), n, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
+                                             D.ptr(ms._steps), D.ptr(ms._applied),
+                                             D.ptr(self.flags) + 4 * first, None, 1,
+                                             t.lsum(gsel * L + first) or None, ledger_out, D.sptr(up)))
+                D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups),
+                                            D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
+                                            D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
+                                            self.n, self.mc_p if self.mc_p else None, buf._dt, hc, up_opts,
+                                            D.sptr(up)))
         mark("rs", rs)
         st.wait_stream(rs)
         st.wait_stream(up)
@@ -449,15 +435,19 @@ class FusedShardedPageStep:
             done = torch.cuda.Event()
             done.record(st)
             self._last_done = done
-        for l in range(L):
-            buf._psel[l] ^= 1
-            buf._version[l] += 1
-            buf._applied_iter[l] = newest[l]
+        t.finish(consumed_flags=False)
         if timings is not None:
             timings["_marks"] = marks
         return list(range(L))
 
-    def step(self, hyper, *, stream=None, timings: dict | None = None):
+    def step(self, hyper, *, stream=None, ag_publish: int = -1, reduce_wide: int = -1,
+             reduce_width: int = -1, timings: dict | None = None):
+        """barrier -> reduce-scatter + check -> barrier -> flag merge ->
+        prologue -> update with the all-gather epilogue -> barrier.  With a
+        host (or SSD) state tier the update streams the owned state pages
+        through HBM staging (the tier's pipeline) between the reduce and the
+        all-gather: each rank moves 24 B x its owned params over its own PCIe
+        link, the 16-bit pages travel over NVLink as usual."""
         buf, ms, lay = self.buffer, self.masters, self.layout
         st = buf._stream(stream)
         L = buf.num_layers
@@ -476,46 +466,47 @@ class FusedShardedPageStep:
                 marks[name] = e
 
         lib, eng = N.lib(), ms._eng
+        clip = getattr(hyper, "max_norm", 0.0) > 0
         with torch.cuda.stream(st):
             mark("start")
             self.flags_local.zero_()
-            if getattr(hyper, "max_norm", 0.0) > 0:
+            if clip:
                 self.sumsq_local.zero_()
             self.h_g.barrier(channel=0)                          # every rank's gradients are complete
+            mark("rs_start")
             gp = self._arr([p + gsel * span_b for p in self.g_ptrs])
             mc = self.mc_g + gsel * span_b if self.mc_g else None
             ch = self._check_chunks
             D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
                                            D.ptr(eng.desc.static(ch)), len(ch), D.ptr(self.flags_local),
-                                           D.ptr(self.sumsq_local), D.sptr(st)))
+                                           D.ptr(self.sumsq_local) if clip else None,
+                                           D.opts(reduce_wide=reduce_wide, reduce_width=reduce_width),
+                                           D.sptr(st)))
             mark("rs")
             self.h_f.barrier(channel=0)                          # flags / norms visible to all
-            clip = getattr(hyper, "max_norm", 0.0) > 0
             D.check(lib.hm_dp_flags_merge(self._arr(self.f_ptrs), self._arr(self.s_ptrs) if clip else None,
                                           self.n, L, D.ptr(self.flags), D.ptr(self.sumsq) if clip else None,
                                           D.sptr(st)))
             mark("check")
-        counts, newest = [], []
+        t = UpdateTicket(buf, range(L), flag_of=lambda l: l)
         for l in range(L):
-            _, c, nw = buf._hand_over(l, st)
-            counts.append(c)
-            newest.append(nw)
-        span = lay.elems16
-        groups = np.zeros(L, dtype=N.GROUP_LAUNCH)
-        for l in range(L):
-            groups[l] = (gsel * span, (psel ^ 1) * span, l, l)
-        dgroups = eng.desc.table(groups)
-        rt = eng.rt_scratch(L)
-        bc, bc_len = ms._bias(hyper, range(L))
-        hc = D.hyper_c(hyper)
-        D.check(lib.hm_adam_prologue(D.ptr(dgroups), L, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
-                                     D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(self.flags),
-                                     D.ptr(self.sumsq), 1, D.sptr(st)))
-        ac = self._adam_chunks
-        D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(ac)), len(ac), D.ptr(dgroups), D.ptr(rt),
-                                    D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool), D.ptr(ms.m32_pool),
-                                    D.ptr(ms.v32_pool), self._arr(self.p_ptrs), self.n,
-                                    self.mc_p if self.mc_p else None, buf._dt, hc, D.sptr(st)))
+            if not self.host_tier:
+                ms._prepub[l] = None
+        dgroups, rt, hc = update_prologue(t, ms, hyper, st, flags=self.flags, sumsq=self.sumsq,
+                                          lsum=t.lsum(gsel * L))
+        peers = self._arr(self.p_ptrs)
+        mcp = self.mc_p if self.mc_p else None
+        up_opts = D.opts(ag_publish=ag_publish)
+
+        def launch(chunks, planes):
+            D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(chunks)), len(chunks), D.ptr(dgroups),
+                                        D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, *planes, peers, self.n,
+                                        mcp, buf._dt, hc, up_opts, D.sptr(st)))
+
+        if self.host_tier:
+            ms.stream_update(range(L), st, lambda chunks, stage: launch(chunks, ms.planes(stage)))
+        else:
+            launch(self._adam_chunks, (D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool)))
         with torch.cuda.stream(st):
             mark("adam")
             self.h_p.barrier(channel=0)                          # published pages landed everywhere
@@ -523,10 +514,7 @@ class FusedShardedPageStep:
             done = torch.cuda.Event()
             done.record(st)
             self._last_done = done
-        for l in range(L):
-            buf._psel[l] ^= 1
-            buf._version[l] += 1
-            buf._applied_iter[l] = newest[l]
+        t.finish(consumed_flags=False)
         if timings is not None:
             timings["_marks"] = marks
         return list(range(L))

@@ -32,7 +32,8 @@ from . import _device as D
 from . import _native as N
 from .errors import ConfigError
 from .layout import PageLayout
-from .lockfree import MasterState, ParamBuffer, SweepResult, _LayerView, _Paged
+from .lockfree import (MasterState, ParamBuffer, SweepResult, UpdateTicket, _LayerView, _Paged,
+                       update_prologue)
 from .pagemem import PAGE_BYTES_DEFAULT
 
 
@@ -51,10 +52,10 @@ class SSDMasterState(_Paged):
 
     def __init__(self, params, path: str, tier: str = "SSD", *, page_bytes: int = PAGE_BYTES_DEFAULT,
                  device=None, layout: PageLayout | None = None, group_pages: int = 64,
-                 slots: int = 3, direct: bool = True, io_threads: int = 4):
-        self._init_paged(params, page_bytes, device, layout)
-        if self.layout.world_size != 1:
-            raise ConfigError("the SSD tier is per process; shard with one layout per rank")
+                 slots: int = 3, direct: bool = True, io_threads: int = 4, world_size: int = 1,
+                 rank: int = 0):
+        # world-sharded: this rank's file holds only the pages it owns (page % N)
+        self._init_paged(params, page_bytes, device, layout, world_size, rank)
         self.tier = tier
         lay = self.layout
         E = lay.E
@@ -113,6 +114,8 @@ class SSDMasterState(_Paged):
             flat = (p.detach().reshape(-1).float().cpu().numpy() if isinstance(p, torch.Tensor)
                     else np.asarray(p, dtype=np.float32).reshape(-1))
             for s in lay.segments[l]:
+                if not lay.owned(s):
+                    continue
                 k, o = self._loc(lay.slot_state(s.page), s.off)
                 by_group.setdefault(k, []).append((o, flat[s.pos:s.pos + s.n]))
         buf = self.pinned[0].numpy()
@@ -139,10 +142,12 @@ class SSDMasterState(_Paged):
     def _file_layer(self, plane: int, layer: int):
         torch.cuda.synchronize(self.device)
         lay = self.layout
-        out = np.empty(lay.numels[layer], dtype=np.float32)
+        out = np.zeros(lay.numels[layer], dtype=np.float32)
         tmp = np.empty(3 * self.gE, dtype=np.float32)
         cache = {}
         for s in lay.segments[layer]:
+            if not lay.owned(s):
+                continue
             k, o = self._loc(lay.slot_state(s.page), s.off)
             if k not in cache:
                 fd = os.open(self.path, os.O_RDONLY)
@@ -173,6 +178,52 @@ class SSDMasterState(_Paged):
 
     _bias = MasterState._bias
 
+    def planes(self, stage) -> tuple[int, int, int]:
+        """Device addresses of the p / m / v planes of an HBM stage."""
+        return D.ptr(stage), D.ptr(stage) + 4 * self.gE, D.ptr(stage) + 8 * self.gE
+
+    def stream_update(self, layers, st, launch, timings=None) -> None:
+        """Stream the state of ``layers`` through the tier: per page group
+        (last first) pread -> H2D -> ``launch(chunks, stage)`` on ``st`` ->
+        D2H -> pwrite, reads running up to S-1 groups ahead; blocks until
+        every group is back in the file.  ``stage`` is laid out [p|m|v]."""
+        plan = self._group_plan(tuple(layers))
+        S, io = self.slots, self.io
+        reads, writes = {}, {}
+
+        def start_read(i):
+            k = plan[i][0]
+            slot = i % S
+            if slot in writes:
+                writes.pop(slot).result()            # slot drained to the drive
+            reads[i] = io.submit(self._pread, k, slot)
+
+        for i in range(min(S - 1, len(plan))):
+            start_read(i)
+        for i, (k, chunks) in enumerate(plan):
+            if i + S - 1 < len(plan):
+                start_read(i + S - 1)
+            reads.pop(i).result()
+            slot, stage = i % S, self.stage[i % 2]
+            self.h2d.wait_stream(self.d2h)     # the HBM stage's previous store finished
+            with torch.cuda.stream(self.h2d):
+                stage.copy_(self.pinned[slot], non_blocking=True)
+                fetched = torch.cuda.Event()
+                fetched.record(self.h2d)
+            st.wait_event(fetched)
+            launch(chunks, stage)
+            updated = torch.cuda.Event()
+            updated.record(st)
+            self.d2h.wait_event(updated)
+            with torch.cuda.stream(self.d2h):
+                self.pinned[slot].copy_(stage, non_blocking=True)
+                stored = torch.cuda.Event()
+                stored.record(self.d2h)
+            writes[slot] = io.submit(self._pwrite, k, slot, stored)
+        for f in writes.values():
+            f.result()
+        st.wait_stream(self.d2h)
+
     def _group_plan(self, layers: tuple):
         """Per group (reverse order): adam chunks with s_off rebased into a
         stage laid out as [p | m | v] planes of gE elements each."""
@@ -200,70 +251,23 @@ def ssd_sweep(buffer: ParamBuffer, masters: SSDMasterState, hyper, layers=None, 
     lay = buffer.layout
     if masters.layout.numels != lay.numels or masters.layout.page_bytes != lay.page_bytes:
         raise ConfigError("buffer and masters were built on different page tables")
+    if lay.world_size != 1:
+        raise ConfigError("a world-sharded SSD tier is updated by the DP step "
+                          "(sharding.FusedShardedPageStep), which all-gathers the published pages")
     st = buffer._stream(stream)
     order = list(reversed(range(buffer.num_layers))) if layers is None else list(layers)
     sel = tuple(l for l in order if buffer._pending[l] > 0)
     if not sel:
         return SweepResult(masters, [], [], [])
-    L, span = buffer.num_layers, lay.elems16
-    rows, counts, newest = [], [], []
-    for l in sel:
-        gbuf, count, new = buffer._hand_over(l, st)
-        rows.append((gbuf * span, (buffer._psel[l] ^ 1) * span, l, gbuf * L + l))
-        counts.append(count)
-        newest.append(new)
-    groups = np.zeros(len(rows), dtype=N.GROUP_LAUNCH)
-    for i, r in enumerate(rows):
-        groups[i] = r
-    eng = masters._eng
-    dgroups = eng.desc.table(groups)
-    rt = eng.rt_scratch(len(rows))
-    bc, bc_len = masters._bias(hyper, sel)
-    hc = D.hyper_c(hyper)
+    t = UpdateTicket(buffer, sel)
+    dgroups, rt, hc = update_prologue(t, masters, hyper, st)
     lib = N.lib()
-    D.check(lib.hm_adam_prologue(D.ptr(dgroups), len(rows), D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
-                                 D.ptr(masters._steps), D.ptr(masters._applied), D.ptr(buffer._flags),
-                                 D.ptr(buffer._sumsq), 1, D.sptr(st)))
-    plan = masters._group_plan(sel)
-    S, gE, io = masters.slots, masters.gE, masters.io
-    reads, writes = {}, {}
 
-    def start_read(i):
-        k = plan[i][0]
-        slot = i % S
-        if slot in writes:
-            writes.pop(slot).result()            # slot drained to the drive
-        reads[i] = io.submit(masters._pread, k, slot)
+    def launch(chunks, stage):
+        D.check(lib.hm_adam_main(D.ptr(masters._eng.desc.static(chunks)), len(chunks), D.ptr(dgroups),
+                                 D.ptr(rt), D.ptr(buffer.g16_pool), buffer._dt, *masters.planes(stage),
+                                 D.ptr(buffer.p16_pool), buffer._dt, hc, None, D.sptr(st)))
 
-    for i in range(min(S - 1, len(plan))):
-        start_read(i)
-    for i, (k, chunks) in enumerate(plan):
-        if i + S - 1 < len(plan):
-            start_read(i + S - 1)
-        reads.pop(i).result()
-        slot, stage = i % S, masters.stage[i % 2]
-        masters.h2d.wait_stream(masters.d2h)     # the HBM stage's previous store finished
-        with torch.cuda.stream(masters.h2d):
-            stage.copy_(masters.pinned[slot], non_blocking=True)
-            fetched = torch.cuda.Event()
-            fetched.record(masters.h2d)
-        st.wait_event(fetched)
-        D.check(lib.hm_adam_main(D.ptr(eng.desc.static(chunks)), len(chunks), D.ptr(dgroups), D.ptr(rt),
-                                 D.ptr(buffer.g16_pool), buffer._dt, D.ptr(stage),
-                                 D.ptr(stage) + 4 * gE, D.ptr(stage) + 8 * gE,
-                                 D.ptr(buffer.p16_pool), buffer._dt, hc, D.sptr(st)))
-        updated = torch.cuda.Event()
-        updated.record(st)
-        masters.d2h.wait_event(updated)
-        with torch.cuda.stream(masters.d2h):
-            masters.pinned[slot].copy_(stage, non_blocking=True)
-            stored = torch.cuda.Event()
-            stored.record(masters.d2h)
-        writes[slot] = io.submit(masters._pwrite, k, slot, stored)
-    for f in writes.values():
-        f.result()
-    for l, new in zip(sel, newest):
-        buffer._psel[l] ^= 1
-        buffer._version[l] += 1
-        buffer._applied_iter[l] = new
-    return SweepResult(masters, sel, counts, newest)
+    masters.stream_update(sel, st, launch)
+    t.finish()
+    return SweepResult(masters, sel, t.counts, t.newest)

@@ -40,7 +40,12 @@ def main():
     mode = os.environ.get("DP_MODE", "nccl")
     buf = LF.ParamBuffer([torch.from_numpy(p) for p in params], dtype=dtype, page_bytes=PAGE,
                          device=dev, layout=lay, pool_alloc=None if mode == "nccl" else symmetric_alloc)
-    ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay)
+    if os.environ.get("DP_HOST", "0") == "1":   # fp32 state in pinned host memory, owned pages only
+        from paper_2303_02868_b200.swap import HostMasterState
+        ms = HostMasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay,
+                             group_pages=2, world_size=world, rank=rank)
+    else:
+        ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay)
     step = ShardedPageStep(buf, ms) if mode == "nccl" else FusedShardedPageStep(buf, ms, mode=mode)
     from paper_2303_02868_b200 import _native as NL
     NL.check(NL.lib().hm_set_ag_publish(int(os.environ.get("DP_AG_PUBLISH", "0"))))

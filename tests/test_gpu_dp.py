@@ -1,7 +1,10 @@
 """Data-parallel page step on >= 2 GPUs (torchrun, NCCL): reduce-scatter of
 the gradient pages, flag all-reduce, sharded page-Adam, all-gather of the
 published pages — checked against the oracle in tests/dp_worker.py.
-Skipped on a single-GPU box (run with `gpurun --gpus 2`)."""
+Every case runs at the largest world the box offers (2, 4 or 8 ranks: the
+north star's one-box width is 8, reference tests/test_acceptance.py:188
+sweeps world in {1, 2, 4, 8}); on a box with more than 2 GPUs a 2-rank
+subset runs as well.  Skipped on a single-GPU box (`gpurun --gpus 2`)."""
 import os
 import subprocess
 import sys
@@ -14,7 +17,7 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("bucket,dtype,mode,groups,ctas", [
+CASES = [
     (1, "bf16", "nccl", 1, 0), (2, "bf16", "nccl", 1, 0), (2, "fp16", "nccl", 1, 0),
     (2, "bf16", "p2p", 1, 0), (2, "fp16", "p2p", 1, 0), (3, "bf16", "nvls", 1, 0),
     (2, "bf16", "p2p", 3, 0), (2, "bf16", "nvls", 4, 0),
@@ -24,10 +27,36 @@ ROOT = Path(__file__).resolve().parent.parent
     (2, "bf16", "p2p", 4, "ingest"),   # host gradient streamed in per group, step starts early
     (2, "bf16", "p2p", 4, "green32"),  # reduce and update in two green contexts (SM partitions)
     (2, "bf16", "p2p", 1, "wide8"), (2, "fp16", "p2p", 3, "wide8"),  # 8-peer reduce kernel
-    (2, "bf16", "p2p", 1, "ld128")])   # the 16 B-load reduce (256-bit loads are the default)
+    (2, "bf16", "p2p", 1, "ld128"),   # the 16 B-load reduce (256-bit loads are the default)
+    (2, "bf16", "p2p", 1, "host"), (3, "fp16", "p2p", 1, "host")]   # fp32 state on the pinned-host tier
+SMOKE2 = [CASES[1], CASES[3], CASES[6], CASES[12], CASES[17]]
+
+
+def _world(n: int) -> int:
+    return 8 if n >= 8 else 4 if n >= 4 else 2
+
+
+@pytest.mark.parametrize("bucket,dtype,mode,groups,ctas", CASES)
 def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
-    agp, upd, ingest, green, width, ld256 = 0, 0, 0, 0, 0, 0
-    if ctas == "ld128":
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    _run(_world(n), bucket, dtype, mode, groups, ctas)
+
+
+@pytest.mark.parametrize("bucket,dtype,mode,groups,ctas", SMOKE2)
+def test_dp_step_two_ranks(bucket, dtype, mode, groups, ctas):
+    n = torch.cuda.device_count()
+    if n <= 2:
+        pytest.skip("the full suite above already ran at world 2")
+    _run(2, bucket, dtype, mode, groups, ctas)
+
+
+def _run(world, bucket, dtype, mode, groups, ctas):
+    agp, upd, ingest, green, width, ld256, host = 0, 0, 0, 0, 0, 0, 0
+    if ctas == "host":
+        host, ctas = 1, 0
+    elif ctas == "ld128":
         ld256, ctas = 1, 0
     elif ctas == "wide8":   # the 8-wide reduce instantiation (what N=8 runs), with a persistent grid when pipelined
         width, ctas = 8, 5
@@ -39,14 +68,13 @@ def test_dp_step_matches_oracle(bucket, dtype, mode, groups, ctas):
         agp, ctas = int(ctas[-1]), 0
     elif isinstance(ctas, str):
         upd, ctas = int(ctas[3:]), 5
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
-    world = 4 if n >= 4 else 2
     env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype, DP_MODE=mode, DP_GROUPS=str(groups),
                DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp),
                DP_UPDATE_CTAS=str(upd), DP_INGEST=str(ingest),
-               DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width))
+               DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width), DP_HOST=str(host))
+    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+    ids = visible.split(",") if visible else [str(i) for i in range(torch.cuda.device_count())]
+    env["CUDA_VISIBLE_DEVICES"] = ",".join(ids[:world])
     if ld256:
         env["DP_REDUCE_WIDE"] = "0"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",

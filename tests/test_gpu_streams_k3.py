@@ -1,0 +1,112 @@
+"""Host-glue concurrency and the accumulate kernel's launch shapes.
+
+* update_layer / sweep on two streams at once: every launch carries its own
+  stream's scratch (prologue runtime table, reject flag) and its own launch
+  settings, so interleaved updates of two MasterStates on two streams are
+  bit-identical to running them one after the other.
+* K3 (hm_accumulate) in its three forms (first messages, adds, per-slot
+  mixed), fp16 and bf16: bit-exact against the oracle's accumulate, with
+  the same reject flags and ledger sums.
+* ingest_sweep(results_to=...): the published pages land in host memory,
+  equal to the device record.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import page_adam as O
+from paper_2303_02868_b200 import lockfree as LF
+
+pytestmark = pytest.mark.gpu
+SIZES = [70001, 1, 5, 32768, 40000, 25003, 777, 65539, 12, 33333]
+PAGE = 64 * 1024
+
+
+def _params(seed):
+    rng = np.random.default_rng(seed)
+    return [torch.from_numpy(rng.normal(0, 0.02, n).astype(np.float32)).cuda() for n in SIZES]
+
+
+def test_update_layer_two_streams_bit_exact(cuda):
+    hyper = LF.AdamHyper(lr=1e-3)
+    rng = np.random.default_rng(3)
+    grads = [[torch.from_numpy(rng.normal(0, 1e-2, n).astype(np.float32)).cuda() for n in SIZES]
+             for _ in range(2)]
+    grads[1][4][7] = float("nan")   # one rejected layer on the second state
+    ref = [LF.MasterState(_params(s), page_bytes=PAGE) for s in (1, 2)]
+    for k in range(2):                               # sequential reference
+        for _ in range(3):
+            for l in reversed(range(len(SIZES))):
+                bool(ref[k].update_layer(l, grads[k][l], hyper))
+    got = [LF.MasterState(_params(s), page_bytes=PAGE) for s in (1, 2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    res = [[], []]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for l in reversed(range(len(SIZES))):        # interleaved launches on two streams
+            for k in range(2):
+                res[k].append(got[k].update_layer(l, grads[k][l], hyper, stream=streams[k]))
+    torch.cuda.synchronize()
+    assert [bool(r) for r in res[1]].count(False) == 3
+    for k in range(2):
+        assert got[k].steps == ref[k].steps
+        for l in range(len(SIZES)):
+            assert torch.equal(got[k].p32[l].view(torch.int32), ref[k].p32[l].view(torch.int32))
+            assert torch.equal(got[k].v32[l].view(torch.int32), ref[k].v32[l].view(torch.int32))
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_accumulate_kinds_bit_exact(cuda, dtype):
+    """The three K3 forms — all first messages, all adds, per-slot mixed —
+    against the oracle's accumulate (lockfree.py:219-220), with the reject
+    flags and the ledger's running sums."""
+    rng = np.random.default_rng(11)
+    L = len(SIZES)
+    buf = LF.ParamBuffer([np.zeros(n, np.float32) for n in SIZES], dtype=dtype, page_bytes=PAGE)
+    acc = [None] * L   # the oracle's 16-bit gradient buffer per layer
+    taken = {2, 5}
+    for it in range(3):
+        if it == 2:                      # mixed: two layers start over after a take
+            for l in taken:
+                buf.take(l)
+                acc[l] = None
+        flat = []
+        for l, n in enumerate(SIZES):
+            g = O.to16((rng.normal(0, 1, n) * 10.0 ** rng.integers(-3, 3, n)).astype(np.float32), dtype)
+            if it == 2 and l == 6:
+                g[9] = O.to16(np.array([np.inf], np.float32), dtype)[0]
+            flat.append(g)
+            base = acc[l] if acc[l] is not None else O.to16(np.zeros(n, np.float32), dtype)
+            acc[l] = O.accumulate16(base, g, dtype)
+        f = np.concatenate(flat)
+        t = torch.from_numpy(f.view(np.int16)).view(torch.bfloat16) if dtype == "bf16" else torch.from_numpy(f)
+        buf.accumulate_flat(t.cuda(), it)
+    want = [O.from16(a, dtype) for a in acc]
+    for l in range(L):
+        got = buf.g16[l]
+        got = O.from16(np.asarray(got).view(np.uint16) if dtype == "bf16" else got, dtype)
+        assert np.array_equal(got.view(np.uint32), want[l].view(np.uint32)), l
+    slot = [buf._gsel[l] * L + l for l in range(L)]
+    flags = buf._flags.cpu().numpy()
+    assert [int(flags[slot[l]]) for l in range(L)] == [int(l == 6) for l in range(L)]
+    sums = buf._lsum.cpu().numpy()
+    for l in range(L):
+        if l != 6:
+            assert sums[slot[l]] == pytest.approx(float(np.sum(want[l].astype(np.float64))),
+                                                  rel=1e-12, abs=1e-12), l
+
+
+def test_ingest_sweep_returns_published_pages(cuda):
+    params = _params(4)
+    buf, ms = LF.ParamBuffer(params, dtype="bf16", page_bytes=PAGE), LF.MasterState(params, page_bytes=PAGE)
+    rng = np.random.default_rng(8)
+    host_out = torch.empty(sum(SIZES), dtype=torch.bfloat16).pin_memory()
+    for it in range(2):
+        g = torch.from_numpy(rng.normal(0, 1e-2, sum(SIZES)).astype(np.float32)).to(torch.bfloat16).pin_memory()
+        LF.ingest_sweep(buf, ms, g, LF.AdamHyper(lr=1e-3), it, groups=3, results_to=host_out)
+        torch.cuda.synchronize()
+        pos = 0
+        for l, n in enumerate(SIZES):
+            assert torch.equal(host_out[pos:pos + n].view(torch.int16),
+                               buf.layer_view(l).cpu().view(torch.int16)), (it, l)
+            pos += n

@@ -1,6 +1,7 @@
 """The C-ABI library loads without a GPU and exports every function that
 include/hm_page.h declares; the ctypes table covers exactly that set."""
 import ctypes
+import ctypes as C
 import re
 from pathlib import Path
 
@@ -26,7 +27,7 @@ def test_library_exports_header():
 
 def test_abi_constants():
     lib = N.lib()
-    assert lib.hm_abi_version() == 1
+    assert lib.hm_abi_version() == 2
     assert lib.hm_device_chunk_elems() == 4096
 
 
@@ -37,6 +38,7 @@ def test_struct_layouts_match_header():
     assert N.GROUP_LAUNCH.names == ("g_shift", "p_shift", "group", "flag")
     assert N.SEG_CHUNK.names == ("src_off", "dst_off", "n", "slot")
     assert ctypes.sizeof(N.AdamHyperC) == 32
+    assert ctypes.sizeof(N.LaunchOpts) == 24 and "typedef struct hm_launch_opts" in text
 
 
 def test_kernels_do_not_spill():
@@ -65,17 +67,29 @@ def test_null_pointers_rejected_before_launch():
     (never a kernel fault), and an empty launch is a no-op."""
     lib = N.lib()
     INVALID = 7
-    assert lib.hm_accumulate(None, 2, None, 2, None, 1, 0, None, None, None, None) == INVALID
+    acc = lambda *a: lib.hm_accumulate(*a, None, None, None, None)
+    assert acc(None, 2, None, 2, None, 1, 0, None, None, None) == INVALID
     assert b"null pointer" in lib.hm_last_error()
     assert lib.hm_cast(None, 3, None, 2, None, 5, None) == INVALID
     assert lib.hm_reduce_stats(None, 2, None, 3, None, None, None, None) == INVALID
     assert lib.hm_copy_runs(None, None, None, 2, None) == INVALID
-    assert lib.hm_accumulate(None, 2, None, 2, None, 0, 0, None, None, None, None) == 0
+    assert acc(None, 2, None, 2, None, 0, 0, None, None, None) == 0
     assert lib.hm_cast(None, 3, None, 2, None, 0, None) == 0
-    assert lib.hm_accumulate(None, 9, None, 2, None, 1, 0, None, None, None, None) == INVALID
+    assert acc(None, 9, None, 2, None, 1, 0, None, None, None) == INVALID
+    assert lib.hm_stats_take(None, 3, None, None, None, None, None) == INVALID
+    assert lib.hm_stats_take(None, 0, None, None, None, None, None) == 0
+    # a ledger delta row without the running sums it telescopes against
+    assert lib.hm_accumulate(None, 2, None, 2, None, 1, 0, None, None, None, None, C.c_void_p(8),
+                             None, None) == INVALID
     assert lib.hm_set_dp_reduce_ctas(-1) == INVALID and lib.hm_set_dp_reduce_ctas(0) == 0
     assert lib.hm_set_ag_publish(3) == INVALID and lib.hm_set_ag_publish(0) == 0
     assert lib.hm_set_adam_threads(300) == INVALID
+    # per-launch options are validated like the process defaults
+    hc = N.AdamHyperC(0.01, 0.9, 0.1, 0.999, 0.001, 1e-8, 1.0, 0.0)
+    assert lib.hm_adam_main(None, 1, None, C.c_void_p(8), None, 2, None, None, None, None, 0, C.byref(hc),
+                            C.byref(N.LaunchOpts(adam_threads=300)), None) == INVALID
+    assert lib.hm_adam_main(None, 1, None, C.c_void_p(8), None, 2, None, None, None, None, 0, C.byref(hc),
+                            C.byref(N.LaunchOpts(adam_variant=5)), None) == INVALID
 
 
 def test_cpulist_parser():

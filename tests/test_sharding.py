@@ -3,7 +3,7 @@
 * the bucketed rank-major slot map is a bijection whose rank-r block of
   every bucket holds exactly the pages owner(p) = p % N assigns to r;
 * PageCollectives' in-place bucketed reduce-scatter / all-gather, run with
-  world_size 2 over gloo, hands every owner the sum of its pages and
+  world_size 2, 4 and 8 over gloo, hands every owner the sum of its pages and
   reassembles the pool (the same calls run over NCCL on the GPU box).
 """
 import os
@@ -98,18 +98,21 @@ def _worker(rank, world, port, K, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("K", [None, 1, 3])
-def test_bucketed_rs_ag_world2_gloo(K):
+@pytest.mark.parametrize("world,K", [(2, None), (2, 1), (2, 3), (4, None), (4, 2), (8, None), (8, 1)])
+def test_bucketed_rs_ag_gloo(world, K):
+    """The reference sweeps world in {1, 2, 4, 8} (tests/test_acceptance.py:188);
+    world 8 is the north star's one-box DP width: same bucket layout,
+    rendezvous and in-place collective plumbing as the NCCL run."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, K, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in procs)
+    res = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: True, 1: True}
+    assert res == {r: True for r in range(world)}
 
 
 def test_modeled_gather_matches_reference_formula():
