@@ -101,27 +101,74 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---- CPU baseline (oracle port of the reference, bounded sample) ---------------------
+# ---- CPU baseline: the reference itself (baseline/_ref) or its oracle port --------
+
+def import_reference():
+    """hiermem from baseline/_ref (the unmodified reference, pip-installed
+    there; git-ignored, shipped to the GPU box with the snapshot), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "hiermem").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import hiermem.lockfree as lf
+        return lf
+    except Exception:
+        return None
+
 
 class CpuReferenceSample:
-    """The reference chain take -> apply_update -> publish cast, restated
-    op-for-op in numpy (oracle/page_adam.py, pinned to the reference), over
-    the first ``sample_pages`` pages' worth of parameters of the workload,
-    fanned out over ``threads`` host threads (numpy ufuncs release the GIL).
-    The synthetic sample is built once; ``run()`` times one pass."""
+    """The reference's update chain over the first ``sample_pages`` pages'
+    worth of parameters of the workload, cut into ``threads`` layers that
+    ``threads`` host threads update concurrently (numpy ufuncs release the
+    GIL).  With the reference installed (baseline/_ref) each layer runs the
+    reference's OWN public calls — ``ParamBuffer.take`` -> ``MasterState.
+    update_layer`` -> ``ParamBuffer.publish(clear=False)`` (hiermem/lockfree.py:
+    624-639), fp16 gradients (its only 16-bit type), one ``accumulate`` per
+    layer before each timed pass (the producer, untimed like the GPU arm's
+    resident gradients); otherwise the same chain restated op for op in numpy
+    (oracle/page_adam.py, pinned bit-exact to it).  ``run()`` times one pass."""
 
     def __init__(self, page_bytes: int, sample_pages: int, threads: int, dtype: str):
         from concurrent.futures import ThreadPoolExecutor
-
-        from oracle import page_adam as O
-        self.O, self.dtype = O, dtype
         self.n = sample_pages * (page_bytes // 2)
-        self.p, self.m, self.v, self.g16 = O.synthetic_layer(0, 0, self.n, dtype, outliers=False)
-        pieces = np.array_split(np.arange(self.n), threads * 4)
+        pieces = np.array_split(np.arange(self.n), threads)
         self.bounds = [(int(a[0]), int(a[-1]) + 1) for a in pieces if len(a)]
         self.pool = ThreadPoolExecutor(max_workers=threads)
+        self.lf = import_reference()
+        rng = np.random.default_rng(0)
+        if self.lf is not None:
+            self.kind, self.dtype = "reference", "fp16"
+            params = [rng.normal(0, 0.02, hi - lo).astype(np.float32) for lo, hi in self.bounds]
+            self.grads = [rng.normal(0, 1e-2, hi - lo).astype(np.float16) for lo, hi in self.bounds]
+            self.buf, self.ms = self.lf.ParamBuffer(params), self.lf.MasterState(params)
+            self.hyper = self.lf.AdamHyper(lr=1e-3)
+            self.it = 0
+        else:
+            from oracle import page_adam as O
+            self.O, self.kind, self.dtype = O, "port", dtype
+            self.p, self.m, self.v, self.g16 = O.synthetic_layer(0, 0, self.n, dtype, outliers=False)
 
-    def _work(self, b):
+    def describe(self) -> str:
+        if self.kind == "reference":
+            return (f"{self.n} params (first pages of the pool) as {len(self.bounds)} layers, one host thread "
+                    "each, running hiermem's own ParamBuffer.take -> MasterState.update_layer -> "
+                    "ParamBuffer.publish(clear=False) (baseline/_ref, hiermem/lockfree.py:624-639), fp16 "
+                    "gradients; the accumulate before each pass is untimed")
+        return (f"{self.n} params (first pages of the pool), {len(self.bounds)} threads; "
+                "take->apply_update->publish restated op-for-op in numpy (oracle/page_adam.py, bit-exact "
+                "to hiermem/lockfree.py:127-263)")
+
+    def _arm(self, l):
+        self.buf.accumulate(self.lf.GradMessage(l, self.grads[l], self.it))
+
+    def _chain(self, l):
+        g, _count, newest = self.buf.take(l)
+        self.ms.update_layer(l, g, self.hyper)
+        self.buf.publish(l, self.ms.p32[l], applied_iter=newest, clear=False)
+
+    def _port(self, b):
         O, lo, hi = self.O, b[0], b[1]
         g = O.from16(self.g16[lo:hi], self.dtype)                                    # take (widen)
         pp, mm, vv, ok = O.adam_update(self.p[lo:hi], self.m[lo:hi], self.v[lo:hi], g,
@@ -130,59 +177,75 @@ class CpuReferenceSample:
         return ok
 
     def run(self) -> float:
+        if self.kind == "reference":
+            L = range(len(self.bounds))
+            list(self.pool.map(self._arm, L))
+            self.it += 1
+            t0 = time.perf_counter()
+            list(self.pool.map(self._chain, L))
+            return time.perf_counter() - t0
         t0 = time.perf_counter()
-        list(self.pool.map(self._work, self.bounds))
+        list(self.pool.map(self._port, self.bounds))
         return time.perf_counter() - t0
 
     def close(self):
         self.pool.shutdown()
 
 
-def cpu_reference_sample(specs, page_bytes, sample_pages: int, threads: int, dtype: str,
+def cpu_reference_sample(page_bytes, sample_pages: int, threads: int, dtype: str,
                          min_seconds: float = 10.0, min_reps: int = 2):
     """Passes over the bounded sample until ``min_seconds`` of CPU work (and
-    at least ``min_reps`` passes) have run; returns (params per pass, median
-    pass time, passes)."""
+    at least ``min_reps`` passes) have run; returns (sample, median pass time,
+    passes)."""
     s = CpuReferenceSample(page_bytes, sample_pages, threads, dtype)
     s.run()  # warm
     times = []
     while len(times) < min_reps or sum(times) < min_seconds:
         times.append(s.run())
     s.close()
-    return s.n, statistics.median(times), len(times)
+    return s, statistics.median(times), len(times)
+
+
+def gpu_config(args, specs, page, layout):
+    """The config dict both arms print: the same keys and values (the driver
+    compares them); arm-specific settings go to the line's "run" key."""
+    from paper_2303_02868_b200 import workloads as W
+    return {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": W.total_elems(specs),
+            "layers": len(specs), "page_bytes": page, "pages": layout.used_pages,
+            "grad_dtype": args.dtype, "parallelism": f"dp{args.gpus}" if args.gpus > 1 else "single GPU",
+            "l2": "inputs larger than L2 (28 B/param x params >> 126 MB)",
+            "step": "take -> update -> publish of every layer's pages (one updating-actor sweep)"}
 
 
 def run_reference(args):
     """--impl reference: the reference's CPU update path on the host cores."""
     from paper_2303_02868_b200 import workloads as W
+    from paper_2303_02868_b200.layout import PageLayout
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     specs = W.config_specs(args.config)
     page = args.page_mib * 2**20 if args.page_mib else W.config_page_bytes(args.config)
     threads = os.cpu_count() or 1
-    E = page // 2
     sample_pages = max(1, min(args.cpu_sample_pages, sum(s.bytes for s in specs) // page))
-    n = sample_pages * E
     sample = CpuReferenceSample(page, sample_pages, threads, args.dtype)
     for _ in range(args.warmup):
         sample.run()
     times = [sample.run() for _ in range(args.steps)]
     sample.close()
     t = statistics.median(times)
-    value = n / t
+    value = sample.n / t
+    layout = PageLayout([s.bytes // 2 for s in specs], page)
+    cfg = gpu_config(args, specs, page, layout)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "params/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "page_bytes": page,
-                   "params": W.total_elems(specs), "grad_dtype": args.dtype},
-        "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads, "kind": "port",
-                         "sample": f"first {sample_pages} pages ({n} params) of the {args.config} pool per step; "
-                                   "take->apply_update->publish restated op-for-op in numpy "
-                                   "(oracle/page_adam.py, bit-exact to hiermem/lockfree.py:127-263)"},
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads, "kind": sample.kind,
+                         "sample": sample.describe() + f"; median of {args.steps} passes"},
         "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "run": {"reference_grad_dtype": sample.dtype, "sample_params": sample.n, "threads": threads},
     }
     print(json.dumps(line), flush=True)
 
@@ -221,12 +284,24 @@ def synthetic_grads(numels, dtype, device, seed):
             for n in numels]
 
 
+def _events(stream, fn, reps: int) -> float:
+    """ms per call of ``fn`` over ``reps`` back-to-back calls (CUDA events)."""
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
 def run_ours_single(args):
     import torch
-    from paper_2303_02868_b200 import lockfree as LF
-    from paper_2303_02868_b200 import workloads as W
-    device = torch.device("cuda", 0)
     from paper_2303_02868_b200 import _device as Dv
+    from paper_2303_02868_b200 import lockfree as LF
+    device = torch.device("cuda", 0)
     numa = Dv.bind_to_gpu_numa(0)   # pinned host buffers next to the GPU's PCIe root
     torch.cuda.set_device(device)
     specs, page, layout, buf, ms = build_state(args, device)
@@ -234,14 +309,15 @@ def run_ours_single(args):
     numels = layout.numels
     P = sum(numels)
     hyper = LF.AdamHyper(lr=1e-3)
+    opts = Dv.opts(adam_threads=args.adam_threads, adam_variant=args.adam_variant)
     # Fill BOTH gradient page buffers through accumulate (K3, which also
-    # computes each layer's finite flag); every step re-offers them, so the
-    # timed region reads gradients already resident in HBM.
+    # computes each layer's finite flag, norm and ledger sum); every step
+    # re-offers them, so the timed region reads gradients already in HBM.
     grads = torch.cat(synthetic_grads(numels, args.dtype, device, 7))  # flat, layer order
     for rnd in range(2):
         buf.accumulate_flat(grads, rnd)
         if rnd == 0:
-            LF.sweep(buf, ms, hyper)
+            LF.sweep(buf, ms, hyper, opts=opts)
 
     def rearm():
         for l in range(L):
@@ -250,7 +326,7 @@ def run_ours_single(args):
     stream = torch.cuda.current_stream(device)
     for _ in range(args.warmup):
         rearm()
-        LF.sweep(buf, ms, hyper)
+        LF.sweep(buf, ms, hyper, opts=opts)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
     with ClockSampler(0) as clk:
@@ -261,7 +337,7 @@ def run_ours_single(args):
         for i in range(args.steps):
             rearm()
             ev[2 * i].record(stream)
-            LF.sweep(buf, ms, hyper)
+            LF.sweep(buf, ms, hyper, opts=opts)
             ev[2 * i + 1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
@@ -272,65 +348,71 @@ def run_ours_single(args):
     peak, peak_kind = load_peaks()
     achieved = BYTES_PER_PARAM * P / (kern_ms / 1e3) / 1e9
 
-    # K3 producer throughput (accumulate into pages, fused finite flag + norm).
-    torch.cuda.synchronize()
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    acc_reps = 5   # back to back, so the host-side launch work overlaps the previous launch
-
+    # K3 producer alone (first message of one flat gradient into every layer's
+    # pages, fused flag + norm + ledger sum), back to back.
     def first_message():
         for l in range(L):
             buf._pending[l] = 0
         buf.accumulate_flat(grads, 0)
-    first_message()
-    torch.cuda.synchronize()
-    a0.record(stream)
-    for _ in range(acc_reps):
+    for _ in range(3):
         first_message()
-    a1.record(stream)
-    torch.cuda.synchronize()
-    acc_ms = a0.elapsed_time(a1) / acc_reps
-    LF.sweep(buf, ms, hyper)
+    acc_ms = _events(stream, first_message, 10)
+    buf._ledger_flush()
 
+    # The whole device step of the updating path: K3 (gradient into pages)
+    # then the fused sweep — 32 B/param (4 B K3 + 28 B update).
+    def device_step():
+        buf.accumulate_flat(grads, 0)
+        LF.sweep(buf, ms, hyper, opts=opts)
+    for _ in range(3):
+        device_step()
+    dev_ms = _events(stream, device_step, 10)
+    buf._ledger_flush()
+
+    three = run_three_call(args, buf, ms, hyper, grads) if args.three_call_steps > 0 else None
     e2e = run_e2e(args, buf, ms, hyper, grads, device) if args.e2e_steps > 0 else None
     traffic = load_traffic(args)
     cpu = None
     Dv.restore_affinity(numa)   # the CPU baseline gets every host core
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        n, t, passes = cpu_reference_sample(specs, page, args.cpu_sample_pages, threads, args.dtype,
-                                            min_seconds=args.cpu_seconds)
-        cpu = {"value": n / t, "unit": "params/s", "cores": threads, "kind": "port",
-               "sample": f"first {args.cpu_sample_pages} pages ({n} params) of the {args.config} pool; "
-                         "take->apply_update->publish restated op-for-op in numpy (oracle/page_adam.py), "
-                         f"{threads} threads, median of {passes} passes (>= {args.cpu_seconds:g} s of CPU work)"}
+        smp, t, passes = cpu_reference_sample(page, args.cpu_sample_pages, threads, args.dtype,
+                                              min_seconds=args.cpu_seconds)
+        cpu = {"value": smp.n / t, "unit": "params/s", "cores": threads, "kind": smp.kind,
+               "sample": smp.describe() + f"; median of {passes} passes (>= {args.cpu_seconds:g} s of CPU work)"}
         # the reference itself is single-threaded numpy: one thread, for context
-        n1, t1, _ = cpu_reference_sample(specs, page, max(1, args.cpu_sample_pages // 8), 1, args.dtype,
-                                         min_seconds=min(2.0, args.cpu_seconds))
-        cpu["single_thread_value"] = n1 / t1
+        one, t1s, _ = cpu_reference_sample(page, max(1, args.cpu_sample_pages // 8), 1, args.dtype,
+                                           min_seconds=min(2.0, args.cpu_seconds))
+        cpu["single_thread_value"] = one.n / t1s
     line = {
         "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": P,
-                   "layers": L, "page_bytes": page, "pages": layout.used_pages,
-                   "adam_threads": args.adam_threads,
-                   "adam_variant": ["ldg", "tma"][args.adam_variant],
-                   "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
-                   "l2": "inputs larger than L2 (28 B/param x params >> 126 MB)",
-                   "step": "fused sweep: prologue + page-Adam over all pages (take->update->publish)"},
+        "config": gpu_config(args, specs, page, layout),
+        "run": {"adam_threads": args.adam_threads, "adam_variant": ["ldg", "tma"][args.adam_variant],
+                "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
+                "kernels": "fused sweep: prologue + page-Adam over all pages"},
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                      "bytes_per_param": BYTES_PER_PARAM, "kernel": "adam_main (+ prologue)",
                      "kernel_ms": kern_ms},
         "accumulate": {"params_per_s": P / (acc_ms / 1e3), "ms": acc_ms,
-                       "gbs": 4 * P / (acc_ms / 1e3) / 1e9, "bytes_per_param": 4,
+                       "gbs": 4 * P / (acc_ms / 1e3) / 1e9, "frac": 4 * P / (acc_ms / 1e3) / 1e9 / peak,
+                       "bytes_per_param": 4,
                        "note": "K3: first-message accumulate of one flat gradient into all layers' "
-                               "pages (read payload, write page) with fused finite flag + squared norm, "
-                               "one launch"},
+                               "pages (read payload, write page) with fused finite flag + squared norm + "
+                               "conservation-ledger sum, one launch"},
+        "device_step": {"params_per_s": P / (dev_ms / 1e3), "ms": dev_ms,
+                        "gbs": 32 * P / (dev_ms / 1e3) / 1e9, "frac": 32 * P / (dev_ms / 1e3) / 1e9 / peak,
+                        "bytes_per_param": 32,
+                        "note": "K3 accumulate + fused sweep, back to back (gradient into pages, then "
+                                "take->update->publish)"},
         "clocks": clk.summary(),
         "gpu_launches": 2 * args.steps,
     }
+    if three:
+        line["three_call"] = three
     if e2e:
         line["e2e"] = e2e
     if cpu:
@@ -338,13 +420,44 @@ def run_ours_single(args):
     print(json.dumps(line), flush=True)
 
 
+def run_three_call(args, buf, ms, hyper, grads):
+    """The reference's own per-layer loop through the drop-in with torch
+    tensors (hiermem/lockfree.py:755-769: take -> update_layer ->
+    publish(clear=False), layers reversed), after the K3 accumulate — to set
+    beside ``device_step`` (K3 + the fused sweep of the same work).  take
+    widens (6 B/param); update_layer reads the taken 16-bit pages in place and
+    pre-publishes (28 B); p32[l] unpacks (8 B); publish only flips: 42 B/param
+    + one K3 (4 B) and ~4 launches per layer."""
+    import torch
+    L = buf.num_layers
+    P = sum(buf.layout.numels)
+
+    def step():
+        buf.accumulate_flat(grads, 0)
+        for l in reversed(range(L)):
+            g, _c, newest = buf.take(l)
+            ms.update_layer(l, g, hyper)
+            buf.publish(l, ms.p32[l], applied_iter=newest, clear=False)
+    for _ in range(2):
+        step()
+    stream = torch.cuda.current_stream()
+    t = _events(stream, step, args.three_call_steps)
+    buf._ledger_flush()
+    return {"params_per_s": P / (t / 1e3), "ms": t, "bytes_per_param": 46,
+            "gbs": 46 * P / (t / 1e3) / 1e9,
+            "api": "accumulate_flat + per layer (reversed): ParamBuffer.take -> MasterState.update_layer -> "
+                   "ParamBuffer.publish(MasterState.p32[l], clear=False), torch tensors"}
+
+
 def run_e2e(args, buf, ms, hyper, grads, device):
     """Public API with host buffers: per step H2D of every layer's gradient
     from pinned memory + accumulate (K3) + fused sweep (K2) + D2H of the
-    per-layer applied flags (the step's result)."""
+    step's result — the freshly published 16-bit parameters of every layer
+    (and the per-layer applied flags)."""
     import torch
     from paper_2303_02868_b200 import lockfree as LF
     host = grads.cpu().pin_memory()
+    out = torch.empty_like(host).pin_memory()
     h2d = host.numel() * host.element_size()
     L = buf.num_layers
 
@@ -353,10 +466,12 @@ def run_e2e(args, buf, ms, hyper, grads, device):
         res = LF.sweep(buf, ms, hyper)     # fused take -> update -> publish (K2)
         return res.applied()               # D2H of the per-layer applied flags
 
-    def pipelined_step():
-        # per layer group: H2D on a copy stream -> K3 -> fused sweep; the
-        # transfer of group k+1 overlaps the update of group k
-        res = LF.ingest_sweep(buf, ms, host, hyper, 0, groups=args.e2e_groups)
+    def pipelined_step(results):
+        # per layer group: H2D on a copy stream -> K3 -> fused sweep -> D2H of
+        # the group's published pages on a second copy stream; the transfer
+        # of group k+1 overlaps the update of group k and the return of k-1
+        res = LF.ingest_sweep(buf, ms, host, hyper, 0, groups=args.e2e_groups,
+                              results_to=out if results else None)
         return res.applied()
 
     def timed(step):
@@ -370,13 +485,19 @@ def run_e2e(args, buf, ms, hyper, grads, device):
         return (time.perf_counter() - t0) / args.e2e_steps
 
     dt_serial = timed(serial_step)
-    dt = timed(pipelined_step)
+    dt_nores = timed(lambda: pipelined_step(False))
+    dt = timed(lambda: pipelined_step(True))
+    buf._ledger_flush()
     P = sum(buf.layout.numels)
+    d2h = out.numel() * out.element_size() + 4 * L
     return {"value": P / dt, "unit": "params/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": 4 * L, "ms_per_step": dt * 1e3, "steps": args.e2e_steps,
-            "api": f"lockfree.ingest_sweep (pinned host gradient, {args.e2e_groups} layer groups)",
-            "h2d_gbs": h2d / dt / 1e9, "serial_ms_per_step": dt_serial * 1e3,
-            "serial_api": "accumulate_flat(host) + sweep"}
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": args.e2e_steps,
+            "api": f"lockfree.ingest_sweep(pinned host gradient, {args.e2e_groups} layer groups, "
+                   "results_to=pinned host params)",
+            "pcie_gbs": (h2d + d2h) / dt / 1e9,
+            "no_results_ms_per_step": dt_nores * 1e3,
+            "serial_ms_per_step": dt_serial * 1e3,
+            "serial_api": "accumulate_flat(host) + sweep (applied flags only)"}
 
 
 def load_traffic(args):
@@ -421,12 +542,15 @@ def main():
                          "(p2p) / NVSwitch multicast (nvls)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--three-call-steps", type=int, default=5,
+                    help="N=1: also time the reference's per-layer take->update_layer->publish loop")
     ap.add_argument("--e2e-groups", type=int, default=8)
     ap.add_argument("--cpu-sample-pages", type=int, default=32)
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="GPU arm's cpu_baseline: repeat the sample for at least this much CPU work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--c3-layers", type=int, default=8, help="C3 slice (host-memory bound)")
+    ap.add_argument("--c3-layers", type=int, default=0,
+                    help="C3 transformer layers (0 = as many of the 40 as the box's host memory holds)")
     ap.add_argument("--c3-lockfree-iters", type=int, default=4,
                     help="C3 host tier: also time sync vs lock-free delayed update (0 = skip)")
     ap.add_argument("--c3-tokens", type=int, default=16384,
@@ -441,15 +565,8 @@ def main():
     ap.add_argument("--ssd-dir", default="/tmp", help="directory of the SSD tier's state file")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    if args.impl != "reference":
-        from paper_2303_02868_b200 import _native
-        _native.check(_native.lib().hm_set_adam_threads(args.adam_threads))
-        _native.check(_native.lib().hm_set_adam_variant(args.adam_variant))
     if args.impl == "reference":
         return run_reference(args)
-    if args.config == "c3":
-        from paper_2303_02868_b200 import swap_bench
-        return swap_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # plain `python bench.py --gpus N`: relaunch as N ranks, one per GPU
@@ -460,6 +577,9 @@ def main():
         os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                                    f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
                                    f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]])
+    if args.config == "c3":
+        from paper_2303_02868_b200 import swap_bench
+        return swap_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks)
     if world > 1 or args.gpus > 1:
         from paper_2303_02868_b200 import dp_bench
         return dp_bench.run(args, METRIC, BYTES_PER_PARAM, ClockSampler, load_peaks, build_state)

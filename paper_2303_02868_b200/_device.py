@@ -136,9 +136,23 @@ def opts(**kw):
     return C.byref(N.LaunchOpts(**kw))
 
 
+_HYPER_C: dict = {}
+
+
 def hyper_c(h) -> N.AdamHyperC:
     """AdamHyper -> f32 scalars with numpy's weak-scalar rounding
-    (lockfree.py:135-141: python float -> f32 per operation)."""
+    (lockfree.py:135-141: python float -> f32 per operation).  Cached per
+    (frozen, hashable) hyper: the struct is only ever read by the library."""
+    try:
+        hit = _HYPER_C.get(h)
+    except TypeError:   # an unhashable stand-in
+        return _hyper_c(h)
+    if hit is None:
+        hit = _HYPER_C[h] = _hyper_c(h)
+    return hit
+
+
+def _hyper_c(h) -> N.AdamHyperC:
     return N.AdamHyperC(
         float(F32(h.lr)), float(F32(h.beta1)), float(F32(1.0 - h.beta1)),
         float(F32(h.beta2)), float(F32(1.0 - h.beta2)), float(F32(h.eps)),

@@ -31,7 +31,10 @@ import torch.distributed as dist
 
 def _init():
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+        from datetime import timedelta
+        # a mismatched collective fails in minutes instead of hanging the box
+        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))),
+                                timeout=timedelta(seconds=int(os.environ.get("HM_DIST_TIMEOUT_S", "300"))))
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -92,9 +95,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     L = len(specs)
     P = sum(layout.numels)
     hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
-    from . import _native as NL
-    NL.check(NL.lib().hm_set_ag_publish(args.ag_publish))
-    NL.check(NL.lib().hm_set_dp_reduce_wide(args.dp_reduce_wide))
+    knobs = {"ag_publish": args.ag_publish, "reduce_wide": args.dp_reduce_wide} if fused else {}
     if args.dp_groups < 0:   # auto: measured policy (profiles/r1_dp_c2.md)
         # pipelining pays at N=2 once the per-group barriers are small next to
         # the transfer (C2/C4/C5, >= 1 GB of 16-bit pages), not for C1 (0.25 GB)
@@ -102,11 +103,12 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         args.dp_groups, args.dp_reduce_ctas = (8, 128) if world == 2 and big else (1, 0)
     pipelined = fused and args.dp_groups > 1
 
-    def do_step(**kw):
+    def do_step(**kw):   # launch settings travel with each launch (hm_launch_opts)
         if pipelined:
             return dp.step_pipelined(hyper, args.dp_groups, reduce_ctas=args.dp_reduce_ctas,
-                                     update_ctas=args.dp_update_ctas, reduce_sms=args.dp_reduce_sms, **kw)
-        return dp.step(hyper, **kw)
+                                     update_ctas=args.dp_update_ctas, reduce_sms=args.dp_reduce_sms,
+                                     **knobs, **kw)
+        return dp.step(hyper, **knobs, **kw)
     flat = owned_grad_flat(layout, args.dtype, device, 7 + rank)
     for rnd in range(2):  # fill both gradient page buffers (K3)
         buf.accumulate_flat(flat, rnd)
@@ -136,20 +138,26 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         dist.barrier()
     step_ms = _max_over_ranks(t0.elapsed_time(t1) / args.steps)
 
-    # Component timings (one instrumented step + isolated collectives).
+    # Phase timings from ONE unpipelined instrumented step (the pipelined
+    # headline overlaps the phases, so its marks cannot be split honestly).
+    rearm()
+    dp.step(hyper, **knobs)    # first use of the unpipelined plan uploads its descriptors
     rearm()
     tm = {}
-    do_step(timings=tm)
+    dp.step(hyper, timings=tm, **knobs)
     torch.cuda.synchronize()
     mk = tm["_marks"]
-    if pipelined:   # reduce of group k+1 overlaps the update of group k: report the spans
-        parts = {"rs_ms": mk["start"].elapsed_time(mk["rs"]), "check_ms": 0.0,
-                 "adam_ms": mk["start"].elapsed_time(mk["adam"]) - mk["start"].elapsed_time(mk["rs"]),
+    if fused:
+        parts = {"barrier_ms": mk["start"].elapsed_time(mk["rs_start"]),
+                 "rs_ms": mk["rs_start"].elapsed_time(mk["rs"]),
+                 "check_ms": mk["rs"].elapsed_time(mk["check"]),
+                 "update_ag_ms": mk["check"].elapsed_time(mk["adam"]),
                  "ag_tail_ms": mk["adam"].elapsed_time(mk["ag"]),
-                 "overlapped_rs_update_ms": mk["start"].elapsed_time(mk["adam"])}
+                 "step_ms": mk["start"].elapsed_time(mk["ag"])}
     else:
         parts = {"rs_ms": mk["start"].elapsed_time(mk["rs"]), "check_ms": mk["rs"].elapsed_time(mk["check"]),
-                 "adam_ms": mk["check"].elapsed_time(mk["adam"]), "ag_tail_ms": mk["adam"].elapsed_time(mk["ag"])}
+                 "update_ms": mk["check"].elapsed_time(mk["adam"]), "ag_tail_ms": mk["adam"].elapsed_time(mk["ag"]),
+                 "step_ms": mk["start"].elapsed_time(mk["ag"])}
     parts = {k: _max_over_ranks(v) for k, v in parts.items()}
     gpool = buf.g16_pool[buf._gsel[0] ^ 1]
     ppool = buf.p16_pool[buf._psel[0]]
@@ -166,63 +174,74 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         torch.cuda.synchronize()
         return _max_over_ranks(a.elapsed_time(b) / reps)
 
-    if fused:  # the collectives live inside the kernels: use the instrumented step
-        rs_ms = parts["rs_ms"]
-        ag_ms = parts["adam_ms"] + parts["ag_tail_ms"]
+    S = 2 * P                                  # the algorithmic 16-bit payload
+    busbw = lambda ms_: S / (ms_ / 1e3) * (world - 1) / world / 1e9
+    if fused:
+        phases = {"rs_ms": parts["rs_ms"], "rs_busbw_gbs": busbw(parts["rs_ms"]),
+                  "update_ag_ms": parts["update_ag_ms"],
+                  "ag_busbw_gbs": busbw(parts["update_ag_ms"]),
+                  "note": "one unpipelined instrumented step: rs = the reduce-scatter+check kernel; "
+                          "ag = the page-Adam kernel whose epilogue stores into every peer (the update's "
+                          "HBM time is inside it)"}
     else:
         rs_ms = timed(lambda: dp.coll.reduce_scatter(gpool))
         ag_ms = timed(lambda: dp.coll.all_gather(ppool))
+        phases = {"rs_ms": rs_ms, "rs_busbw_gbs": busbw(rs_ms), "ag_ms": ag_ms, "ag_busbw_gbs": busbw(ag_ms),
+                  "note": "NCCL collectives timed alone"}
+    link = measure_nvlink(device, world, rank)
     pipe = None
     if fused:
         pipe = lambda ready: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
                                                ready=ready)
     e2e = run_e2e(args, buf, ms, do_step, flat, layout, pipe) if args.e2e_steps > 0 else None
-    # busbw counts the ALGORITHMIC bytes S = 2 B x params; the
-    # padded pool (whole buckets) is larger, but the fused kernels never move
-    # the padding and NCCL's extra bytes are overhead, not useful traffic
-    pool_bytes = layout.elems16 * 2
-    S = 2 * P
-    busbw = lambda ms_: S / (ms_ / 1e3) * (world - 1) / world / 1e9
-    # Sharded page-Adam alone (owned pages) for the HBM roofline.
+    # Link-level bytes per direction per GPU for the step: P2P (and NCCL)
+    # move (N-1)/N*S in for the reduce-scatter and (N-1)/N*S in for the
+    # all-gather (the same out); NVLS reads the reduced S/N from the switch
+    # and receives the multicast (N-1)/N*S, so S per direction.
+    nvls = fused and args.dp_mode == "nvls"
+    link_bytes = S if nvls else 2 * S * (world - 1) / world
+    peak = link["ingress_gbs"]
+    achieved = link_bytes / (step_ms / 1e3) / 1e9
     owned = layout.owned_numel()
-    # pipelined: the update kernels overlap the reduce, so only the whole span bounds them
-    adam_ms = parts["overlapped_rs_update_ms"] if pipelined else parts["adam_ms"]
-    peak, peak_kind = load_peaks()
-    achieved = bytes_per_param * owned / (adam_ms / 1e3) / 1e9 if adam_ms > 0 else None
+    peak_hbm, peak_kind = load_peaks()
+    upd_ms = parts["update_ag_ms"] if fused else parts["update_ms"]
     line = {
         "metric": metric, "value": P / (step_ms / 1e3), "unit": "params/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {W.CONFIGS[args.config][2]}", "params": P, "layers": L,
-                   "page_bytes": page, "pages": layout.used_pages, "bucket_pages_per_rank": layout.K,
-                   "buckets": layout.num_buckets, "parallelism": f"dp{world} (page-sharded ZeRO-3)",
-                   "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
-                   "l2": "inputs larger than L2",
-                   "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
-                   "dp_groups": args.dp_groups if pipelined else 1,
-                   "dp_reduce_ctas": args.dp_reduce_ctas if pipelined else 0,
-                   "dp_update_ctas": args.dp_update_ctas if pipelined else 0,
-                   "dp_reduce_sms": args.dp_reduce_sms if pipelined else 0,
-                   "ag_publish": ["per-thread stores", "bulk", "bulk+wait"][args.ag_publish],
-                   "step": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
+                   "page_bytes": page, "pages": layout.used_pages, "grad_dtype": args.dtype,
+                   "parallelism": f"dp{world}", "l2": "inputs larger than L2 (28 B/param x params >> 126 MB)",
+                   "step": "take -> update -> publish of every layer's pages (one updating-actor sweep)"},
+        "run": {"bucket_pages_per_rank": layout.K, "buckets": layout.num_buckets,
+                "sharding": "page-sharded ZeRO-3 (owner = page % N)",
+                "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
+                "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
+                "dp_groups": args.dp_groups if pipelined else 1,
+                "dp_reduce_ctas": args.dp_reduce_ctas if pipelined else 0,
+                "dp_update_ctas": args.dp_update_ctas if pipelined else 0,
+                "dp_reduce_sms": args.dp_reduce_sms if pipelined else 0,
+                "ag_publish": ["per-thread stores", "bulk", "bulk"][args.ag_publish],
+                "kernels": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
                             "page-Adam(bucket) || AG(bucket)") if not fused else
                            ("barrier -> fused reduce-scatter+check over peer memory -> barrier -> "
                             "flag merge -> prologue -> page-Adam with all-gather epilogue -> barrier")},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "peak_kind": peak_kind,
-                     "traffic": None, "kernel": ("adam_main on owned pages (instrumented step, "
-                                                 "overlapped with AG)") if not pipelined else
-                                                ("reduce+update span of the layer-group pipeline "
-                                                 "(adam_main overlapped with RS and AG)"), "kernel_ms": adam_ms},
-        "nvlink": {"rs_ms": rs_ms, "ag_ms": ag_ms,
-                   "note": ("isolated NCCL collectives" if not fused else
-                            "fused kernels: rs = reduce+check kernel; ag = page-Adam with the all-gather "
-                            "epilogue (includes the update) + final barrier"), "rs_busbw_gbs": busbw(rs_ms), "ag_busbw_gbs": busbw(ag_ms),
-                   "peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                   "nominal_gbs": 900.0, "rs_frac": busbw(rs_ms) / 770.0, "ag_frac": busbw(ag_ms) / 770.0,
-                   "algorithmic_bytes": S, "pool_bytes_padded": pool_bytes,
-                   "link_bound_ms": 2 * S * (world - 1) / world / 770e9 * 1e3},
+        "roofline": {"bound": "nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_kind": "measured on this box: " + link["how"],
+                     "bytes_per_step": link_bytes,
+                     "bytes_rule": ("S per direction per GPU (NVLS: reduced S/N from the switch + the "
+                                    "multicast (N-1)/N*S)") if nvls else
+                                   "2(N-1)/N * S per direction per GPU (RS in + AG in), S = 2 B x params",
+                     "link_bound_ms": link_bytes / peak / 1e6,
+                     "kernel": "whole DP step (reduce-scatter, update, all-gather)"},
+        "hbm": {"update_kernel_ms": upd_ms, "owned_params": owned,
+                "gbs": 28 * owned / (upd_ms / 1e3) / 1e9 if upd_ms > 0 else None, "peak": peak_hbm,
+                "peak_kind": peak_kind, "note": "owned-page update of the unpipelined instrumented step (the "
+                                                "fused kernel also pushes the all-gather over NVLink)"},
+        "nvlink": dict(phases, peak_gbs=peak, nominal_gbs=900.0, link=link, algorithmic_bytes=S,
+                       pool_bytes_padded=layout.elems16 * 2),
         "components_ms": parts,
         "reference_model": _reference_model(layout, page, world),
         "clocks": clk.summary(),
@@ -235,6 +254,42 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def measure_nvlink(device, world, rank, nbytes: int = 1 << 29, reps: int = 5) -> dict:
+    """Per-GPU NVLink ingress measured on this box: every rank pulls a
+    ``nbytes`` block from each peer in turn (copy-engine peer reads of a
+    symmetric buffer, peers visited in rank-rotated order), all ranks at
+    once — the traffic pattern of the reduce-scatter / all-gather.  Also the
+    one-pair, one-direction copy for context."""
+    import torch.distributed._symmetric_memory as symm
+    buf = symm.empty(nbytes, dtype=torch.uint8, device=device)
+    h = symm.rendezvous(buf, dist.group.WORLD.group_name)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    peers = [h.get_buffer((rank + k) % world, (nbytes,), torch.uint8) for k in range(1, world)]
+    st = torch.cuda.current_stream(device)
+
+    def pull(which, active=True):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps if active else 0):
+            for pv in which:
+                dst.copy_(pv)
+        b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+    pull(peers)   # warm
+    t_all = _max_over_ranks(pull(peers))
+    # one pair, one direction: rank 0 pulls from rank 1 while the others idle
+    # (every rank still takes part in the barrier and the reduction)
+    t_pair = _max_over_ranks(pull(peers[:1], active=(rank == 0)))
+    pair = nbytes / (t_pair / 1e3) / 1e9
+    ingress = (world - 1) * nbytes / (t_all / 1e3) / 1e9
+    return {"ingress_gbs": ingress, "pair_gbs": pair,
+            "how": f"copy-engine peer reads, every rank pulling {nbytes >> 20} MiB from each peer at once, "
+                   "slowest rank"}
 
 
 def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):

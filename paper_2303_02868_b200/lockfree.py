@@ -297,10 +297,21 @@ def adam_launch(engine: _Engine, chunks: np.ndarray, groups: np.ndarray, g, g_dt
         D.sptr(stream)))
 
 
+_ROWS: dict = {}
+
+
 def _group_rows(rows) -> np.ndarray:
-    a = np.zeros(len(rows), dtype=N.GROUP_LAUNCH)
-    for i, (gs, ps, grp, flag) in enumerate(rows):
-        a[i] = (gs, ps, grp, flag)
+    """hm_group_launch table of (g_shift, p_shift, group, flag) rows (cached:
+    the per-layer calls of the three-call path repeat the same few rows)."""
+    key = tuple(rows)
+    a = _ROWS.get(key)
+    if a is None:
+        a = np.zeros(len(rows), dtype=N.GROUP_LAUNCH)
+        for i, (gs, ps, grp, flag) in enumerate(rows):
+            a[i] = (gs, ps, grp, flag)
+        if len(_ROWS) > 4096:
+            _ROWS.clear()
+        _ROWS[key] = a
     return a
 
 
@@ -513,7 +524,10 @@ class MasterState(_Paged):
     def _unpack(self, pool, layer, stream=None):
         st = self._stream(stream)
         with torch.cuda.stream(st):
-            out = torch.zeros(self.layout.numels[layer], dtype=torch.float32, device=self.device)
+            # world 1: every element is written by the unpack; sharded: the
+            # pages other ranks own read as zeros
+            alloc = torch.empty if self.layout.world_size == 1 else torch.zeros
+            out = alloc(self.layout.numels[layer], dtype=torch.float32, device=self.device)
         self._cast(pool, N.DT_F32, out, N.DT_F32,
                    self.layout.seg_chunks(layer, "state", owned_only=True, reverse=True), st)
         return self._out(out, layer)

@@ -17,6 +17,7 @@ from __future__ import annotations
 import json
 import os
 import time
+from collections.abc import Sequence
 
 import torch
 
@@ -87,46 +88,110 @@ def measure_drive(path: str, nbytes: int = 2 << 30, block: int = 64 << 20):
             "path": os.path.dirname(os.path.abspath(path))}
 
 
+class LazyParams(Sequence):
+    """Per-layer random f32 parameters generated on the device on demand (one
+    layer alive at a time): the 13B model's 51 GB of initial fp32 values
+    never sit in host memory next to its 154 GB of pinned state."""
+
+    def __init__(self, numels, device, seed: int = 1234):
+        self.numels, self.device, self.seed = list(numels), device, seed
+
+    def __len__(self):
+        return len(self.numels)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        g = torch.Generator(device=self.device)
+        g.manual_seed(self.seed * 1_000_003 + i)
+        return torch.empty(self.numels[i], dtype=torch.float32, device=self.device).normal_(0, 0.02, generator=g)
+
+
+def fit_layers(requested: int, world: int) -> tuple[int, dict]:
+    """Transformer layers of C3 whose pinned fp32 state (12 B/param, split over
+    the ranks of this box) fits the box's host memory, at most 40."""
+    from . import workloads as W
+    per_layer = W.total_elems(W.gpt_param16(W.GPTShape(2048, 5120, 20480, 1), embeddings=False))
+    emb = W.total_elems(W.gpt_param16(W.GPTShape(2048, 5120, 20480, 0), embeddings=True))
+    avail = 0
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    avail = int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    budget = avail - (12 << 30) - world * (6 << 30)   # OS + per-rank process, CUDA context, transients
+    fit = max(1, min(40, int((budget - 12 * emb) // (12 * per_layer)))) if avail else 8
+    layers = fit if requested <= 0 else min(requested, 40)
+    return layers, {"mem_available_gb": avail / 1e9, "state_budget_gb": budget / 1e9, "layers_that_fit": fit}
+
+
 def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
     from . import lockfree as LF
     from . import workloads as W
     from .layout import PageLayout
-    device = torch.device("cuda", 0)
-    torch.cuda.set_device(device)
-    shape = W.GPTShape(2048, 5120, 20480, args.c3_layers)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from .dp_bench import _init, _max_over_ranks
+        rank, world, device = _init()
+    else:
+        rank, device = 0, torch.device("cuda", 0)
+        torch.cuda.set_device(device)
+    from . import _device as Dv
+    numa = Dv.bind_to_gpu_numa(device.index)
+    layers, mem = fit_layers(args.c3_layers, world)
+    shape = W.GPTShape(2048, 5120, 20480, layers)
     specs = W.gpt_param16(shape)
     full_params = W.total_elems(W.config_specs("c3"))
     page = args.page_mib * 2**20 if args.page_mib else W.config_page_bytes("c3")
     numels = [s.bytes // 2 for s in specs]
-    layout = PageLayout(numels, page, names=[s.name for s in specs])
-    gen = torch.Generator(device=device)
-    gen.manual_seed(1234)
-    params = [torch.empty(n, dtype=torch.float32, device=device).normal_(0, 0.02, generator=gen)
-              for n in numels]
-    buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout)
+    layout = PageLayout(numels, page, world_size=world, rank=rank, names=[s.name for s in specs])
+    params = LazyParams(numels, device)
+    pool_alloc = None
+    if world > 1:
+        from .sharding import symmetric_alloc
+        pool_alloc = symmetric_alloc
+    buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout,
+                         pool_alloc=pool_alloc)
     t0 = time.perf_counter()
     ssd_path = None
     if args.state_tier == "ssd":
         from .ssd import SSDMasterState, ssd_sweep as sweep_fn
         ssd_path = os.path.join(args.ssd_dir, f"hm_state_{os.getpid()}.bin")
         hm = SSDMasterState(params, ssd_path, page_bytes=page, device=device, layout=layout,
-                            group_pages=args.swap_group_pages, slots=max(3, args.swap_slots))
+                            group_pages=args.swap_group_pages, slots=max(3, args.swap_slots),
+                            world_size=world, rank=rank)
     else:
         from .swap import HostMasterState, swap_sweep as sweep_fn
         hm = HostMasterState(params, page_bytes=page, device=device, layout=layout,
-                             group_pages=args.swap_group_pages, slots=args.swap_slots)
+                             group_pages=args.swap_group_pages, slots=args.swap_slots,
+                             world_size=world, rank=rank)
     init_s = time.perf_counter() - t0
     del params
     torch.cuda.empty_cache()
     P = sum(numels)
-    gen.manual_seed(7)
-    tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
-    grads = torch.empty(P, dtype=torch.float32, device=device).normal_(0, 1e-2, generator=gen).to(tdt)
-    hyper = LF.AdamHyper(lr=1e-3)
+    owned = layout.owned_numel()
+    hyper = LF.AdamHyper(lr=1e-3, inv_scale=1.0 / world)
+    if world > 1:
+        from .dp_bench import owned_grad_flat
+        from .sharding import FusedShardedPageStep
+        grads = owned_grad_flat(layout, args.dtype, device, 7 + rank)
+        dp = FusedShardedPageStep(buf, hm)
+        step = lambda: dp.step(hyper)
+    else:
+        gen = torch.Generator(device=device)
+        gen.manual_seed(7)
+        tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
+        grads = torch.empty(P, dtype=tdt, device=device)
+        for a in range(0, P, 1 << 28):   # in slices: no 51 GB f32 temporary
+            b = min(P, a + (1 << 28))
+            grads[a:b] = torch.empty(b - a, device=device).normal_(0, 1e-2, generator=gen).to(tdt)
+        step = lambda: sweep_fn(buf, hm, hyper)
     for rnd in range(2):
         buf.accumulate_flat(grads, rnd)
         if rnd == 0:
-            sweep_fn(buf, hm, hyper)
+            step()
     L = len(specs)
 
     def rearm():
@@ -135,23 +200,28 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
 
     for _ in range(args.warmup):
         rearm()
-        sweep_fn(buf, hm, hyper)
+        step()
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     stream = torch.cuda.current_stream(device)
-    with ClockSampler(0) as clk:
+    with ClockSampler(device.index) as clk:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t_wall = time.perf_counter()
         a.record(stream)
         for _ in range(args.steps):
             rearm()
-            sweep_fn(buf, hm, hyper)
+            step()
         b.record(stream)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
     # the SSD sweep blocks on host I/O, so its step time is the wall clock
     ms_step = (t_wall * 1e3 if args.state_tier == "ssd" else a.elapsed_time(b)) / args.steps
-    moved = 24 * P  # 12 B fetched + 12 B stored per param
+    if world > 1:
+        ms_step = _max_over_ranks(ms_step)
+    moved = 24 * owned  # 12 B fetched + 12 B stored per owned param, per rank
     achieved = moved / (ms_step / 1e3) / 1e9
     if args.state_tier == "ssd":
         hm.close()
@@ -162,30 +232,52 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
                 "peak_kind": "measured sequential pread/pwrite (harmonic mean of read and write) "
                              "on the same file system", "bytes_per_param": 24, "drive": drive}
     else:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()   # every rank measures at once: the host memory is shared
         pcie = measure_pcie(device)
-        roof = {"bound": "pcie", "achieved": achieved, "peak": pcie["bidir_gbs"], "unit": "GB/s",
-                "frac": achieved / pcie["bidir_gbs"], "peak_kind": "measured pinned cudaMemcpyAsync "
-                "H2D||D2H on this box", "bytes_per_param": 24, "pcie": pcie}
+        peak = pcie["bidir_gbs"] if world == 1 else _min_over_ranks(pcie["bidir_gbs"])
+        roof = {"bound": "pcie", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_kind": "measured pinned cudaMemcpyAsync H2D||D2H on this box" +
+                (", all ranks at once, slowest rank" if world > 1 else ""),
+                "bytes_per_param": 24, "per": "rank (its owned pages over its own PCIe link)", "pcie": pcie}
     lockfree = None
-    if args.state_tier == "host" and args.c3_lockfree_iters > 0:
+    if world == 1 and args.state_tier == "host" and args.c3_lockfree_iters > 0:
         lockfree = _lockfree(args, buf, hm, hyper, grads, P, device)
     line = {
-        "metric": metric, "value": P / (ms_step / 1e3), "unit": "params/s", "n_gpus": 1,
+        "metric": metric, "value": P / (ms_step / 1e3), "unit": "params/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"c3: GPT-3 13B page pools, first {args.c3_layers} of 40 layers + "
-                               f"embeddings; fp32 state on the {args.state_tier} tier",
+        "config": {"workload": f"c3: GPT-3 13B page pools, {layers} of 40 layers + embeddings; fp32 state "
+                               f"on the {args.state_tier} tier" + (", page-sharded over ranks" if world > 1 else ""),
                    "params": P, "full_model_params": full_params, "layers": L, "page_bytes": page,
                    "pages": layout.used_pages, "group_pages": args.swap_group_pages,
                    "staging_slots": args.swap_slots, "state_gb": 12 * P / 1e9,
-                   "init_s": init_s, "full_model_step_ms_extrapolated": ms_step * full_params / P},
+                   "state_gb_per_rank": 12 * owned / 1e9, "parallelism": f"dp{world}" if world > 1 else "single GPU",
+                   "host_memory": mem, "init_s": init_s,
+                   "full_model_step_ms_extrapolated": ms_step * full_params / P,
+                   "step": "swap sweep: per page group H2D -> page-Adam -> D2H" if world == 1 else
+                           "DP step: fused reduce-scatter -> prologue -> per owned page group H2D -> "
+                           "page-Adam with all-gather epilogue -> D2H"},
         "roofline": roof,
         "clocks": clk.summary(),
-        "gpu_launches": args.steps * (1 + hm.num_groups),
+        "gpu_launches": args.steps * (1 + hm.num_groups + (4 if world > 1 else 0)),
     }
     if lockfree:
         line["lockfree"] = lockfree
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _min_over_ranks(x: float) -> float:
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return float(t.item())
 
 
 def _lockfree(args, buf, hm, hyper, grads, P, device):

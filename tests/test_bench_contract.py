@@ -24,7 +24,21 @@ def test_reference_arm_line():
     assert d["warmup"] >= 3 and d["steps"] == 1
     assert d["metric"] == json.loads((ROOT / "BASELINE.json").read_text())["metric"]
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
+    # the reference itself when baseline/_ref holds it, else the oracle port
+    want = "reference" if (ROOT / "baseline" / "_ref" / "hiermem").exists() else "port"
+    assert cb["kind"] == want and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("c1")
+
+
+def test_both_arms_print_the_same_config():
+    """The GPU arm's config is built by the same function (bench.gpu_config),
+    so the driver's same-config check compares like with like."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", ROOT / "bench.py")
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    src = (ROOT / "bench.py").read_text()
+    assert src.count('"config": gpu_config(args, specs, page, layout)') == 1   # the GPU arm
+    assert "cfg = gpu_config(args, specs, page, layout)" in src               # the reference arm
