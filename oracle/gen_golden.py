@@ -17,6 +17,8 @@ Outputs
                            C1..C5 (param16 specs in a GPU pool)
   toy_sync.json            reference run_sync(ZERO) / reference_train loss
                            curves for the whole-chain equivalence test
+  inventory_param16.json   param16 specs of the reference's tensor_inventory
+                           for C1, C2, C3, C5
 """
 from __future__ import annotations
 
@@ -145,6 +147,21 @@ def pagetable_configs():
         json.dump(configs, f)
 
 
+def inventories():
+    """param16 lists of the reference's tensor_inventory (hiermem/footprint.py:
+    184-219) for the GPT configs of BASELINE.json (C1, C2, C3, C5): the
+    fixture tests/test_workloads.py pins workloads.config_specs against."""
+    shapes = {"c1": (1024, 768, 3072, 12, 12), "c2": (2048, 2048, 8192, 24, 16),
+              "c3": (2048, 5120, 20480, 40, 40), "c5": (2048, 12288, 49152, 1, 96)}
+    out = {}
+    for name, (seq, d, f, layers, heads) in shapes.items():
+        cfg = footprint.TransformerConfig(1, seq, d, f, layers, heads)
+        out[name] = [[s.name, s.kind, s.bytes, s.layer_index] for s in footprint.tensor_inventory(cfg)
+                     if s.kind == "param16"]
+    with open(GOLDEN / "inventory_param16.json", "w") as fh:
+        json.dump(out, fh)
+
+
 def toy_sync():
     cfg = lockfree.ToyTrainConfig(num_layers=3, dim=16, batch_size=32, seed=5, noise_std=1.0)
     ref = lockfree.reference_train(cfg, 25)
@@ -210,6 +227,7 @@ if __name__ == "__main__":
     adam_cases()
     pagetable_random()
     pagetable_configs()
+    inventories()
     toy_sync()
     schedules()
     print("golden fixtures written to", GOLDEN)

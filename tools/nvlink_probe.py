@@ -110,20 +110,20 @@ def main():
         x["flags"].zero_()
         D.check(lib.hm_dp_reduce_check(arr(g_ptrs), n, None, D.ptr(buf.g16_pool[0]), buf._dt,
                                        D.ptr(eng.desc.static(x["check"])), len(x["check"]),
-                                       D.ptr(x["flags"]), D.ptr(x["sumsq"]), D.sptr(x["stream"])))
+                                       D.ptr(x["flags"]), D.ptr(x["sumsq"]), None, D.sptr(x["stream"])))
 
     def upd(x):
         eng, buf, ms = x["ms"]._eng, x["buf"], x["ms"]
         dgroups = eng.desc.table(x["groups"])
-        rt = eng.rt_scratch(x["L"])
+        rt = eng.rt_scratch(x["L"], x["stream"])
         bc, bc_len = ms._bias(hyper, range(x["L"]))
         D.check(lib.hm_adam_prologue(D.ptr(dgroups), x["L"], D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
                                      D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(x["flags"]),
-                                     None, 1, D.sptr(x["stream"])))
+                                     None, 1, None, None, D.sptr(x["stream"])))
         D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(x["adam"])), len(x["adam"]), D.ptr(dgroups),
                                     D.ptr(rt), D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
                                     D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), arr(p_ptrs), n, None,
-                                    buf._dt, hc, D.sptr(x["stream"])))
+                                    buf._dt, hc, None, D.sptr(x["stream"])))
 
     sync_all()
     rs_ms, up_ms = [], []

@@ -38,29 +38,29 @@ def main():
         g[l] = (0, lay.elems16, l, l)
     eng, lib = ms._eng, N.lib()
     adam = lay.adam_chunks(range(L), "pool", owned_only=True)
-    dgroups, rt = eng.desc.table(g), eng.rt_scratch(L)
+    st = torch.cuda.current_stream(dev)
+    dgroups, rt = eng.desc.table(g), eng.rt_scratch(L, st)
     hyper = LF.AdamHyper(lr=1e-3)
     hc = D.hyper_c(hyper)
     bc, bc_len = ms._bias(hyper, range(L))
     flags = torch.zeros(L, dtype=torch.int32, device=dev)
-    st = torch.cuda.current_stream(dev)
     own = (C.c_uint64 * 1)(D.ptr(buf.p16_pool))
     times = {}
     for name in ("local", "peer_self", "local", "peer_self"):
         D.check(lib.hm_adam_prologue(D.ptr(dgroups), L, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
                                      D.ptr(ms._steps), D.ptr(ms._applied), D.ptr(flags), None, 1,
-                                     D.sptr(st)))
+                                     None, None, D.sptr(st)))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         if name == "local":
             D.check(lib.hm_adam_main(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups), D.ptr(rt),
                                      D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool), D.ptr(ms.m32_pool),
-                                     D.ptr(ms.v32_pool), D.ptr(buf.p16_pool), buf._dt, hc, D.sptr(st)))
+                                     D.ptr(ms.v32_pool), D.ptr(buf.p16_pool), buf._dt, hc, None, D.sptr(st)))
         else:
             D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups), D.ptr(rt),
                                         D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool),
                                         D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), own, 1, None, buf._dt,
-                                        hc, D.sptr(st)))
+                                        hc, None, D.sptr(st)))
         b.record(st)
         torch.cuda.synchronize()
         times[name] = a.elapsed_time(b)
