@@ -179,6 +179,15 @@ __device__ __forceinline__ void decode(const Raw8<DT>& r, F8& out) {
 
 __device__ __forceinline__ bool is_finite(float x) { return isfinite(x); }
 
+// A buffer base the 8-element vector path may use: 16 B aligned for the
+// 16-bit types (128-bit accesses), 32 B for f32 (256-bit accesses).  With an
+// element offset that is a multiple of 8 the access is then aligned.  The
+// kernels fall back to scalar element access otherwise, so any base works.
+template <int DT>
+__device__ __forceinline__ bool vec_base(const void* p) {
+  return ((uintptr_t)p & (DT == HM_DT_F32 ? 31u : 15u)) == 0;
+}
+
 // Deterministic block reduction of a double (fixed tree order).
 template <int NT>
 __device__ __forceinline__ double block_sum(double x, double* smem) {

@@ -182,7 +182,9 @@ __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
   s.bc2 = r.bc2;
   s.gscale = r.gscale;
 
-  const bool vec = ((go | so | po | (uint64_t)n) & (kVec - 1)) == 0;
+  const bool vec = ((go | so | po | (uint64_t)n) & (kVec - 1)) == 0 && vec_base<GDT>(g) &&
+                   vec_base<HM_DT_F32>(p32) && vec_base<HM_DT_F32>(m32) && vec_base<HM_DT_F32>(v32) &&
+                   (PDT == 0 || PUB != kPubLocal || vec_base<PDT>(p16));
   if (vec) {
     // Issue every load of the thread's 2 granules before any math: 2 x
     // (16 B g + 3 x 32 B state) in flight per thread.

@@ -157,7 +157,10 @@ adam_tma(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
         const hm_adam_chunk c = chunks[blockIdx.x + it * gridDim.x];
         const hm_group_launch gl = groups[c.slot];
         const uint64_t go = c.g_off + gl.g_shift, so = c.s_off, po = c.p_off + gl.p_shift;
-        const bool vec = ((go | so | po | (uint64_t)c.n) & (kVec - 1)) == 0;
+        // bulk copies need 16 B aligned global addresses and sizes
+        const bool vec = ((go | so | po | (uint64_t)c.n) & (kVec - 1)) == 0 && vec_base<GDT>(g) &&
+                         vec_base<HM_DT_F32>(p32) && vec_base<HM_DT_F32>(m32) && vec_base<HM_DT_F32>(v32) &&
+                         (PDT == 0 || vec_base<PDT>(p16));
         vecflag[s] = vec ? 1 : 0;
         unsigned char* st = smem + s * L::kBytes;
         if (vec) {

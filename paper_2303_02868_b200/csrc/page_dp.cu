@@ -108,7 +108,8 @@ __device__ __forceinline__ void reduce_chunks(const hm_seg_chunk* __restrict__ c
       c[m].n = 0;
       c[m].slot = 0;
     }
-    vec[m] = ((c[m].src_off | (uint64_t)c[m].n) & (kVec - 1)) == 0;
+    vec[m] = ((c[m].src_off | (uint64_t)c[m].n) & (kVec - 1)) == 0 && vec_base<DT>(local) &&
+             (MC ? vec_base<DT>(mc) : true);   // peer bases: checked by make_peers
   }
 #pragma unroll
   for (int m = 0; m < M; ++m) {
@@ -218,7 +219,11 @@ reduce_check_wide_kernel(const hm_seg_chunk* __restrict__ chunks, int n_chunks, 
   static_assert(kChunk == kThreads * 16, "16 elements per thread");
   const hm_seg_chunk c = chunks[blockIdx.x];
   const uint64_t off = c.src_off;
-  if (((off | (uint64_t)c.n) & 15) != 0) {
+  bool wide_ok = ((uintptr_t)local & 31u) == 0;
+#pragma unroll
+  for (int r = 0; r < NP; ++r)
+    if (r < peers.n) wide_ok &= (peers.p[r] & 31u) == 0;
+  if (((off | (uint64_t)c.n) & 15) != 0 || !wide_ok) {
     reduce_chunks<DT, false, NP, 1>(chunks, blockIdx.x, n_chunks, peers, mc, local, nonfinite, sumsq);
     return;
   }
@@ -319,7 +324,14 @@ int make_peers(const uint64_t* ptrs, int n, PeerPtrs* out) {
   if (n < 1 || n > kMaxPeers || !ptrs)
     return hm_set_error(HM_ERR_INVALID, "peer count %d outside 1..%d", n, kMaxPeers);
   out->n = n;
-  for (int i = 0; i < kMaxPeers; ++i) out->p[i] = i < n ? ptrs[i] : 0;
+  for (int i = 0; i < kMaxPeers; ++i) {
+    out->p[i] = i < n ? ptrs[i] : 0;
+    // peer pools are symmetric allocations (page aligned); the 16 B vector
+    // loads/stores to them assume at least that
+    if (i < n && (ptrs[i] & 15u) != 0)
+      return hm_set_error(HM_ERR_INVALID, "peer buffer %d at %#llx is not 16-byte aligned", i,
+                          (unsigned long long)ptrs[i]);
+  }
   return HM_OK;
 }
 

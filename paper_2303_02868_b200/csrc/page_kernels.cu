@@ -141,7 +141,8 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
   bool bad = false;
   float sq = 0.f;
   LedgerAcc<LM> ls;
-  const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
+  const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0 &&
+                   vec_base<SDT>(src) && vec_base<DDT>(dst);
   if (vec) {
     Raw8<SDT> ra[kSegVecPer];
     Raw8<DDT> rb[KIND == 0 ? 1 : kSegVecPer];
@@ -225,7 +226,8 @@ cast_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ sr
             void* __restrict__ dst) {
   const hm_seg_chunk c = chunks[blockIdx.x];
   const int tid = threadIdx.x;
-  const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0;
+  const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0 &&
+                   vec_base<SDT>(src) && vec_base<DDT>(dst);
   if (vec) {
     Raw8<SDT> ra[kSegVecPer];
 #pragma unroll
@@ -257,7 +259,7 @@ reduce_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ 
   const int tid = threadIdx.x;
   bool bad = false;
   double s = 0.0, sq = 0.0;
-  const bool vec = ((c.src_off | (uint64_t)c.n) & (kVec - 1)) == 0;
+  const bool vec = ((c.src_off | (uint64_t)c.n) & (kVec - 1)) == 0 && vec_base<SDT>(src);
   if (vec) {
     Raw8<SDT> ra[kSegVecPer];
 #pragma unroll

@@ -1,0 +1,161 @@
+"""Out-of-bounds write guards for every data-path kernel.
+
+compute-sanitizer is closed on this GPU pool (runs under it left GPUs
+needing a reset), so the memory-safety evidence is our own: every page pool
+the kernels write (16-bit gradient / publish pools, fp32 p/m/v state) is a
+view into a larger allocation whose guard bands before and after hold a
+sentinel bit pattern.  All kernel forms then run — K3 in its three forms,
+the fused sweep with 256 / 512 threads and the TMA bulk-copy variant, the
+take -> update_layer -> publish fast path, and the DP kernels (reduce-
+scatter in both load widths, as a persistent grid and 8-wide; flag merge;
+update with the per-thread and the staged bulk-copy all-gather epilogue and
+the persistent update grid) with the local pools standing in for every
+peer — and every guard band must be bit-identical afterwards, and the
+results equal to the plain sweep's.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2303_02868_b200 import _device as D
+from paper_2303_02868_b200 import _native as N
+from paper_2303_02868_b200 import lockfree as LF
+
+pytestmark = pytest.mark.gpu
+SIZES = [70001, 1, 5, 32768, 40000, 25003, 777, 12, 33333]
+PAGE = 64 * 1024
+PAD = 3 * 4096 + 64         # guard elements per side (keeps the pools 128-byte aligned, as the
+                            # caching allocator does: the vector paths assume aligned bases)
+SENTINEL = {torch.bfloat16: 0x7F81, torch.float16: 0x7E01, torch.float32: 0x7FC0_1234}
+
+
+class Guarded:
+    """Allocator returning views into padded buffers with sentinel guards."""
+
+    def __init__(self):
+        self.bufs = []
+
+    def __call__(self, shape, dtype, device):
+        n = int(np.prod(shape))
+        idt = torch.int16 if dtype != torch.float32 else torch.int32
+        big = torch.full((n + 2 * PAD,), SENTINEL[dtype], dtype=idt, device=device)
+        self.bufs.append((big, idt))
+        return big[PAD:PAD + n].view(dtype).view(*shape)
+
+    def adopt(self, t: torch.Tensor) -> torch.Tensor:
+        """A guarded copy of an existing pool tensor."""
+        g = self(t.shape, t.dtype, t.device)
+        g.copy_(t)
+        return g
+
+    def intact(self) -> bool:
+        torch.cuda.synchronize()
+        ok = True
+        for big, idt in self.bufs:
+            want = big[:1]   # the sentinel value, as stored
+            ok &= bool((big[:PAD] == want).all()) and bool((big[-PAD:] == want).all())
+        return ok
+
+
+def _state(dtype, guard, seed=0):
+    rng = np.random.default_rng(seed)
+    params = [torch.from_numpy(rng.normal(0, 0.02, n).astype(np.float32)).cuda() for n in SIZES]
+    buf = LF.ParamBuffer(params, dtype=dtype, page_bytes=PAGE, pool_alloc=guard)
+    ms = LF.MasterState(params, page_bytes=PAGE)
+    if guard is not None:
+        ms.p32_pool, ms.m32_pool, ms.v32_pool = (guard.adopt(ms.p32_pool), guard.adopt(ms.m32_pool),
+                                                 guard.adopt(ms.v32_pool))
+    return buf, ms
+
+
+def _dp_self(buf, ms, hyper):
+    lib, eng = N.lib(), ms._eng
+    lay, L = buf.layout, buf.num_layers
+    st = torch.cuda.current_stream()
+    arr = lambda ptrs: (C.c_uint64 * len(ptrs))(*ptrs)
+    check = lay.pool_chunks(range(L), "16", owned_only=True)
+    adam = lay.adam_chunks(range(L), "pool", owned_only=True)
+    flags = torch.zeros(L, dtype=torch.int32, device=buf.device)
+    sumsq = torch.zeros(L, dtype=torch.float64, device=buf.device)
+    merged = torch.zeros(L, dtype=torch.int32, device=buf.device)
+    g = buf.g16_pool[buf._gsel[0]]
+    for o in (D.opts(reduce_wide=1), D.opts(reduce_wide=0), D.opts(grid_ctas=5), D.opts(reduce_width=8)):
+        D.check(lib.hm_dp_reduce_check(arr([D.ptr(g)]), 1, None, D.ptr(g), buf._dt,
+                                       D.ptr(eng.desc.static(check)), len(check), D.ptr(flags),
+                                       D.ptr(sumsq), o, D.sptr(st)))
+    D.check(lib.hm_dp_flags_merge(arr([D.ptr(flags)]), arr([D.ptr(sumsq)]), 1, L, D.ptr(merged),
+                                  D.ptr(sumsq), D.sptr(st)))
+    rows = np.zeros(L, dtype=N.GROUP_LAUNCH)
+    for l in range(L):
+        rows[l] = (buf._gsel[0] * lay.elems16, (buf._psel[0] ^ 1) * lay.elems16, l, l)
+    dgroups = eng.desc.table(rows, st)
+    rt = eng.rt_scratch(L, st)
+    hc = D.hyper_c(hyper)
+    for o in (D.opts(ag_publish=0), D.opts(ag_publish=1), D.opts(grid_ctas=7)):
+        bc, bc_len = ms._bias(hyper, range(L))
+        D.check(lib.hm_adam_prologue(D.ptr(dgroups), L, D.ptr(rt), hc, D.ptr(bc), bc_len, 0, D.ptr(ms._steps),
+                                     D.ptr(ms._applied), D.ptr(merged), None, 1, None, None, D.sptr(st)))
+        D.check(lib.hm_adam_main_ag(D.ptr(eng.desc.static(adam)), len(adam), D.ptr(dgroups), D.ptr(rt),
+                                    D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool), D.ptr(ms.m32_pool),
+                                    D.ptr(ms.v32_pool), arr([D.ptr(buf.p16_pool)]), 1, None, buf._dt, hc,
+                                    o, D.sptr(st)))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_no_kernel_writes_outside_its_pools(cuda, dtype):
+    hyper = LF.AdamHyper(lr=1e-3)
+    guard = Guarded()
+    results = []
+    for g in (guard, None):
+        buf, ms = _state(dtype, g)
+        rng = np.random.default_rng(1)
+        flat = torch.from_numpy(rng.normal(0, 1e-2, sum(SIZES)).astype(np.float32)).cuda().to(D.TORCH16[dtype])
+        buf.accumulate_flat(flat, 0)                   # first-message form
+        buf.accumulate_flat(flat, 1)                   # add form
+        buf.take(2)
+        buf.accumulate_flat(flat, 2)                   # mixed form
+        for threads, variant in ((256, 0), (512, 0), (256, 1)):
+            LF.sweep(buf, ms, hyper, opts=D.opts(adam_threads=threads, adam_variant=variant))
+            buf.accumulate_flat(flat, 3)
+        gr, _, newest = buf.take(4)                    # the three-call fast path
+        ms.update_layer(4, gr, hyper)
+        buf.publish(4, ms.p32[4], applied_iter=newest, clear=False)
+        LF.sweep(buf, ms, hyper)
+        buf.accumulate_flat(flat, 4)
+        _dp_self(buf, ms, hyper)
+        torch.cuda.synchronize()
+        results.append((ms.p32_pool.clone(), buf.p16_pool.clone()))
+    assert guard.intact(), "a kernel wrote into a guard band"
+    assert torch.equal(results[0][0].view(torch.int32), results[1][0].view(torch.int32))
+    assert torch.equal(results[0][1].view(torch.int16), results[1][1].view(torch.int16))
+
+
+def test_misaligned_buffers_take_the_scalar_path(cuda):
+    """A gradient or parameter tensor that is a view at an odd element offset
+    (so its base is not 16/32-byte aligned) is still updated bit-exactly:
+    the kernels check base alignment and fall back to element access
+    instead of issuing misaligned vector loads."""
+    from oracle import page_adam as O
+    rng = np.random.default_rng(4)
+    n = 9000
+    p = rng.normal(0, 0.02, n).astype(np.float32)
+    m = rng.normal(0, 1e-3, n).astype(np.float32)
+    v = np.square(rng.normal(0, 1e-3, n)).astype(np.float32)
+    g16 = O.to16(rng.normal(0, 1e-2, n).astype(np.float32), "fp16")
+    big = torch.zeros(n + 1, dtype=torch.float16, device="cuda")
+    big[1:] = torch.from_numpy(g16).cuda()
+    grad = big[1:]                                        # base 2 bytes past an aligned block
+    assert grad.data_ptr() % 16 != 0
+    hyper = LF.AdamHyper(lr=1e-3)
+    pp, mm, vv, ok = LF.apply_update(torch.from_numpy(p).cuda(), torch.from_numpy(m).cuda(),
+                                     torch.from_numpy(v).cuda(), grad, hyper, 7)
+    rp, rm, rv, rok = O.adam_update(p, m, v, O.from16(g16, "fp16"), 1e-3, 0.9, 0.999, 1e-8, 7)
+    assert ok and rok
+    assert np.array_equal(pp.cpu().numpy().view(np.uint32), rp.view(np.uint32))
+    assert np.array_equal(vv.cpu().numpy().view(np.uint32), rv.view(np.uint32))
+    # accumulate of a misaligned payload
+    buf = LF.ParamBuffer([np.zeros(n, np.float32)], page_bytes=PAGE)
+    buf.accumulate(LF.GradMessage(0, grad, 0))
+    assert np.array_equal(np.asarray(buf.g16[0]).view(np.uint16), g16.view(np.uint16))
