@@ -15,6 +15,8 @@ import numpy as np
 from .errors import AllocationError, ConfigError, MoveError, NativeError, ProtocolError
 
 LIB_PATH = Path(__file__).resolve().parent / "libhm_page.so"
+if os.environ.get("HM_LIB_VARIANT"):   # measurement builds only (tools/build_variants.sh)
+    LIB_PATH = LIB_PATH.with_name(f"libhm_page_{os.environ['HM_LIB_VARIANT']}.so")
 
 HM_OK, HM_ERR_CONFIG, HM_ERR_ALLOCATION, HM_ERR_MOVE, HM_ERR_PROTOCOL, HM_ERR_KEY, \
     HM_ERR_CUDA, HM_ERR_INVALID = range(8)

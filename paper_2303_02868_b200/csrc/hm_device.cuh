@@ -69,6 +69,19 @@ __device__ __forceinline__ void st_stream_f8(float* p, const F8& r) {
       : "memory");
 }
 
+// 256-bit access of 16 sixteen-bit elements (read-only source, evict-first).
+__device__ __forceinline__ void ld_ro_u8(const void* p, uint32_t (&u)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void st_u8(void* p, const uint32_t (&u)[8]) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(u[0]),
+               "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7])
+               : "memory");
+}
+
 // ---- typed element access (widen exactly / narrow with RNE) ---------------
 template <int DT>
 struct Elem;
@@ -91,6 +104,19 @@ struct Elem<HM_DT_F32> {
   static __device__ __forceinline__ float widen(T x) { return x; }
   static __device__ __forceinline__ T narrow(float x) { return x; }
 };
+
+// 16-bit element <-> its bit pattern (16-bit DT only).
+template <int DT>
+__device__ __forceinline__ float widen_bits(uint16_t b) {
+  using T = typename Elem<DT>::T;
+  return Elem<DT>::widen(*reinterpret_cast<const T*>(&b));
+}
+template <int DT>
+__device__ __forceinline__ uint32_t narrow_bits(float x) {
+  using T = typename Elem<DT>::T;
+  const T h = Elem<DT>::narrow(x);
+  return (uint32_t)(*reinterpret_cast<const uint16_t*>(&h));
+}
 
 template <int DT>
 __device__ __forceinline__ float load1(const void* base, uint64_t off) {

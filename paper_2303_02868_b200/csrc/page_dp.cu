@@ -300,19 +300,25 @@ RcFn pick_rc_np(bool persistent) {
                     : reduce_check_kernel<DT, false, NP, 1>;
 }
 
+// Multicast reduce as a persistent grid: one in-switch load per granule and
+// chunk, so a CTA can keep more chunks in flight than the P2P form at the
+// same register cost (the layer-group pipeline gives it a few SMs only).
+constexpr int kMcDepth = 4;
+
 template <int DT>
 RcFn pick_rc_dt(bool mc, int n, bool persistent) {
   // multicast: one in-switch load per granule; NP still bounds the P2P loads of
   // the unaligned head/tail chunks, which are summed peer by peer
-  if (mc) return reduce_check_kernel<DT, true, kMaxPeers, 1>;
+  if (mc) return persistent ? reduce_check_kernel<DT, true, kMaxPeers, kMcDepth>
+                            : reduce_check_kernel<DT, true, kMaxPeers, 1>;
   if (n <= 2) return pick_rc_np<DT, 2>(persistent);
   if (n <= 4) return pick_rc_np<DT, 4>(persistent);
   return pick_rc_np<DT, 8>(persistent);
 }
 
 RcFn pick_rc(int dt, bool mc, int n, bool persistent, int* depth) {
-  *depth = !persistent || mc ? 1 : n <= 2 ? persistent_depth<2>() : n <= 4 ? persistent_depth<4>()
-                                                                              : persistent_depth<8>();
+  *depth = !persistent ? 1 : mc ? kMcDepth : n <= 2 ? persistent_depth<2>() : n <= 4 ? persistent_depth<4>()
+                                                                                      : persistent_depth<8>();
   if (dt == HM_DT_BF16) return pick_rc_dt<HM_DT_BF16>(mc, n, persistent);
   if (dt == HM_DT_F16) return pick_rc_dt<HM_DT_F16>(mc, n, persistent);
   return nullptr;

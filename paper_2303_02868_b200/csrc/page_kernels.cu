@@ -116,16 +116,30 @@ struct LedgerAcc<2> {
 //
 // One 4096-element chunk per CTA, every raw load of the thread issued before
 // any decode.  KIND: 0 = every chunk is a first message (the common case:
-// one message per step; only the source is read, 16 data registers, so 32
-// registers per thread and 16 CTAs = 64 warps per SM — ncu on C2: register-
-// limited occupancy (40 warps) left the loads latency-bound at 60% of DRAM
-// peak); 1 = every chunk adds; 2 = per-slot mode from slot_modes.  More
+// one message per step; only the source is read — ncu on C2: round 1's
+// 48-register kernel was register-limited to 40 warps per SM and latency-
+// bound at 60% of DRAM peak; this form runs 12 CTAs of 40 registers with
+// 32 B accesses); 1 = every chunk adds; 2 = per-slot mode from slot_modes.  More
 // chunks per CTA with the same bytes in flight measured 50% slower (fewer
 // resident CTAs to overlap the store and epilogue phases).
+// The 32 B first-message path (HM_K3_WIDE=0 at build time restores the
+// 16 B-access form for measurement: tools/build_variants.sh).
+#ifndef HM_K3_WIDE
+#define HM_K3_WIDE 1
+#endif
+constexpr bool kWideK3 = HM_K3_WIDE != 0;
+
+// First-message form between 16-bit buffers: 12 resident CTAs (40 registers,
+// no spill) measured best — 16 CTAs force 32 registers and spill the
+// compensated ledger sum (C2, ledger on: 0.840-0.846 ms vs 0.861-0.913; the
+// 16 B-access form at 16 CTAs: 0.852).
+#ifndef HM_K3_MINB
+#define HM_K3_MINB 12
+#endif
 template <int SDT, int DDT>
 constexpr int acc_min_blocks(int kind) {
   // f32 granules are 32 B (twice the registers of a 16-bit granule)
-  return SDT == HM_DT_F32 || DDT == HM_DT_F32 ? (kind == 0 ? 8 : 4) : (kind == 0 ? 16 : 8);
+  return SDT == HM_DT_F32 || DDT == HM_DT_F32 ? (kind == 0 ? 8 : 4) : (kind == 0 ? HM_K3_MINB : 8);
 }
 
 template <int SDT, int DDT, int KIND, int LM>
@@ -143,6 +157,57 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
   LedgerAcc<LM> ls;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0 &&
                    vec_base<SDT>(src) && vec_base<DDT>(dst);
+  // First messages between 16-bit buffers: 32 B accesses (16 elements) —
+  // half the load/store instructions of the 16 B path, and the source read
+  // carries the L2 evict-first hint (256-bit accesses only, sm_100a).  Chunks
+  // whose offsets / count / bases do not allow it (segment heads and tails)
+  // take the element path: keeping the 16 B path in the same kernel would
+  // cost registers, i.e. resident CTAs, for every chunk.
+  constexpr bool k16 = SDT != HM_DT_F32 && DDT != HM_DT_F32;
+  if constexpr (KIND == 0 && k16 && kWideK3) {
+    const bool wide = ((c.src_off | c.dst_off | (uint64_t)c.n) & 15) == 0 &&
+                      (((uintptr_t)src | (uintptr_t)dst) & 31u) == 0;
+    if (wide) {
+      using TS = typename Elem<SDT>::T;
+      using TD = typename Elem<DDT>::T;
+      constexpr int kW = kChunk / (kSegThreads * 16);   // 2 wide granules per thread
+      uint32_t ra[kW][8];
+#pragma unroll
+      for (int k = 0; k < kW; ++k) {
+        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * 16;
+        if (e < c.n) ld_ro_u8(static_cast<const TS*>(src) + c.src_off + e, ra[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < kW; ++k) {
+        const uint32_t e = (uint32_t)(k * kSegThreads + tid) * 16;
+        if (e >= c.n) continue;
+        // converted in place: element j of the output overwrites element j
+        // of the input once it has been read (both types are 16-bit)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          uint32_t& w = ra[k][j >> 1];
+          const uint16_t bits = (j & 1) ? (uint16_t)(w >> 16) : (uint16_t)(w & 0xffffu);
+          const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(0.0f, widen_bits<SDT>(bits))));
+          bad |= !is_finite(r);
+          sq += __fmul_rn(r, r);
+          if constexpr (LEDGER) ls.add(r);
+          const uint32_t ob = narrow_bits<DDT>(r);
+          w = (j & 1) ? ((w & 0xffffu) | (ob << 16)) : ((w & 0xffff0000u) | ob);
+        }
+        st_u8(static_cast<TD*>(dst) + c.dst_off + e, ra[k]);
+      }
+    } else {
+      for (uint32_t i = tid; i < c.n; i += kSegThreads) {
+        const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(0.0f, load1<SDT>(src, c.src_off + i))));
+        bad |= !is_finite(r);
+        sq += __fmul_rn(r, r);
+        if constexpr (LEDGER) ls.add(r);
+        store1<DDT>(dst, c.dst_off + i, r);
+      }
+    }
+    flush_stats<LEDGER, false>(bad, sq, ls.total(), nonfinite, sumsq, lsum, ldelta, c.slot);
+    return;
+  }
   if (vec) {
     Raw8<SDT> ra[kSegVecPer];
     Raw8<DDT> rb[KIND == 0 ? 1 : kSegVecPer];
