@@ -12,6 +12,7 @@ struct PeerPtrs {
   int n;
 };
 
-int make_peers(const uint64_t* ptrs, int n, PeerPtrs* out);
+// align: required alignment of every peer address (16 for page pools)
+int make_peers(const uint64_t* ptrs, int n, PeerPtrs* out, unsigned align = 16);
 
 }  // namespace hm

@@ -326,17 +326,18 @@ RcFn pick_rc(int dt, bool mc, int n, bool persistent, int* depth) {
 
 }  // namespace
 
-int make_peers(const uint64_t* ptrs, int n, PeerPtrs* out) {
+int make_peers(const uint64_t* ptrs, int n, PeerPtrs* out, unsigned align) {
   if (n < 1 || n > kMaxPeers || !ptrs)
     return hm_set_error(HM_ERR_INVALID, "peer count %d outside 1..%d", n, kMaxPeers);
   out->n = n;
   for (int i = 0; i < kMaxPeers; ++i) {
     out->p[i] = i < n ? ptrs[i] : 0;
     // peer pools are symmetric allocations (page aligned); the 16 B vector
-    // loads/stores to them assume at least that
-    if (i < n && (ptrs[i] & 15u) != 0)
-      return hm_set_error(HM_ERR_INVALID, "peer buffer %d at %#llx is not 16-byte aligned", i,
-                          (unsigned long long)ptrs[i]);
+    // loads/stores to them assume at least that (flag / norm arrays: their
+    // element size)
+    if (i < n && (ptrs[i] & (align - 1)) != 0)
+      return hm_set_error(HM_ERR_INVALID, "peer buffer %d at %#llx is not %u-byte aligned", i,
+                          (unsigned long long)ptrs[i], align);
   }
   return HM_OK;
 }
@@ -400,9 +401,9 @@ int hm_set_dp_reduce_ctas(int ctas) {
 int hm_dp_flags_merge(const uint64_t* peer_flags, const uint64_t* peer_sumsq, int n_peers,
                       int n_layers, uint32_t* flags_out, double* sumsq_out, void* stream) {
   hm::PeerPtrs f, s;
-  if (int rc = hm::make_peers(peer_flags, n_peers, &f)) return rc;
+  if (int rc = hm::make_peers(peer_flags, n_peers, &f, 4)) return rc;
   if (peer_sumsq) {
-    if (int rc = hm::make_peers(peer_sumsq, n_peers, &s)) return rc;
+    if (int rc = hm::make_peers(peer_sumsq, n_peers, &s, 8)) return rc;
   } else {
     s = f;
     sumsq_out = nullptr;
