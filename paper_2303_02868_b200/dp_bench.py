@@ -191,8 +191,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     link = measure_nvlink(device, world, rank)
     pipe = None
     if fused:
-        pipe = lambda ready: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
-                                               ready=ready)
+        pipe = lambda ready, out: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
+                                                    ready=ready, results_to=out, **knobs)
     e2e = run_e2e(args, buf, ms, do_step, flat, layout, pipe) if args.e2e_steps > 0 else None
     # Link-level bytes per direction per GPU for the step: P2P (and NCCL)
     # move (N-1)/N*S in for the reduce-scatter and (N-1)/N*S in for the
@@ -305,7 +305,9 @@ def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
                crossing PCIe (fused mode only).  The headline is the faster."""
     from . import lockfree as LF
     host = flat.cpu().pin_memory()
+    out = torch.empty_like(host).pin_memory()
     h2d = host.numel() * host.element_size()
+    d2h = 2 * layout.owned_numel()      # this rank's published pages
 
     def serial(it):
         buf.accumulate_flat(host, it)      # H2D (non_blocking from pinned) + K3
@@ -314,7 +316,7 @@ def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
 
     def pipelined(it):
         ready = LF.ingest(buf, host, it, groups=args.e2e_groups)
-        pipe(ready)
+        pipe(ready, out)
         return ms._applied.cpu()
 
     def timed(step):
@@ -332,14 +334,17 @@ def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
     dt_pipe = timed(pipelined) if pipe is not None else None
     dt = min(dt_serial, dt_pipe) if dt_pipe else dt_serial
     P = sum(layout.numels)
+    piped = bool(dt_pipe and dt_pipe <= dt_serial)
     return {"value": P / dt, "unit": "params/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": 4 * len(layout.numels), "ms_per_step": dt * 1e3,
+            "d2h_bytes_per_step": (d2h if piped else 0) + 4 * len(layout.numels), "ms_per_step": dt * 1e3,
+            "bytes_note": "per rank; the ranks' D2H pieces are disjoint (the whole model returns once)",
             "steps": args.e2e_steps, "h2d_gbs_per_rank": h2d / dt / 1e9,
             "serial_ms_per_step": dt_serial * 1e3,
             "pipelined_ms_per_step": dt_pipe * 1e3 if dt_pipe else None,
             "api": ("lockfree.ingest(pinned host gradient, %d layer groups) -> "
-                    "FusedShardedPageStep.step_pipelined(ready=...) -> applied flags to host, every rank"
-                    % args.e2e_groups) if dt_pipe and dt_pipe <= dt_serial else
+                    "FusedShardedPageStep.step_pipelined(ready=..., results_to=pinned host params: this "
+                    "rank's owned published pages) -> applied flags to host, every rank"
+                    % args.e2e_groups) if piped else
                    "ParamBuffer.accumulate_flat(pinned host gradient) + sharded page step + "
                    "applied flags to host, every rank"}
 

@@ -1168,21 +1168,27 @@ def ingest_sweep(buffer: ParamBuffer, masters: MasterState, host_grad, hyper: Ad
     return _MultiResult(masters, parts)
 
 
-def _publish_to_host(buffer: ParamBuffer, grp, host, starts, st, d2h) -> None:
+def _publish_to_host(buffer: ParamBuffer, grp, host, starts, st, d2h, *, owned_only: bool = False,
+                     pbuf=None) -> None:
     """D2H of the published pages of layer group ``grp`` into the flat host
     tensor: one cudaMemcpyAsync per contiguous run of the pool (layers
     allocated in order are one run), queued on ``d2h`` behind the group's
-    update on ``st``."""
+    update on ``st``.  ``owned_only``: only this rank's pages (a DP step's
+    ranks return disjoint pieces); ``pbuf``: the publish buffer to read
+    (default: each layer's current record)."""
     lay = buffer.layout
     cache = buffer.__dict__.setdefault("_d2h_runs", {})
-    key = (tuple(grp), tuple(buffer._psel[l] for l in grp))
+    sel = tuple(buffer._psel[l] if pbuf is None else pbuf for l in grp)
+    key = (tuple(grp), sel, owned_only)
     if key not in cache:
         runs = []
         E, esz = lay.E, 2
-        for l in grp:
+        for l, b in zip(grp, sel):
             base = int(starts[l])
             for s in lay.segments[l]:
-                src = (buffer._psel[l] * lay.elems16 + lay.slot16(s.page) * E + s.off) * esz
+                if owned_only and not lay.owned(s):
+                    continue
+                src = (b * lay.elems16 + lay.slot16(s.page) * E + s.off) * esz
                 dst = (base + s.pos) * esz
                 if runs and runs[-1][0] + runs[-1][2] == src and runs[-1][1] + runs[-1][2] == dst:
                     runs[-1][2] += s.n * esz
@@ -1190,6 +1196,8 @@ def _publish_to_host(buffer: ParamBuffer, grp, host, starts, st, d2h) -> None:
                     runs.append([src, dst, s.n * esz])
         cache[key] = np.array([tuple(r) for r in runs], dtype=N.COPY_DESC)
     runs = cache[key]
+    if not len(runs):
+        return
     ev = torch.cuda.Event()
     ev.record(st)
     d2h.wait_event(ev)

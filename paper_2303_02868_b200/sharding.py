@@ -314,7 +314,7 @@ class FusedShardedPageStep:
 
     def step_pipelined(self, hyper, groups: int = 4, *, reduce_ctas: int = 0, update_ctas: int = 0,
                        reduce_sms: int = 0, ready=None, stream=None, ag_publish: int = -1,
-                       reduce_wide: int = -1, reduce_width: int = -1,
+                       reduce_wide: int = -1, reduce_width: int = -1, results_to=None,
                        timings: dict | None = None):
         """``step`` with the layers cut into contiguous groups and two streams:
         the reduce-scatter + check of group k+1 runs while group k is updated
@@ -334,7 +334,11 @@ class FusedShardedPageStep:
         in per GPU) and the AG leg inbound-heavy (S/N out, S in), so
         overlapping them moves (1 + 1/N)·S per link direction instead of
         2·(N−1)/N·S.  Launch settings travel with each launch (hm_launch_opts),
-        nothing process-wide is changed."""
+        nothing process-wide is changed.  ``results_to`` (pinned host, every
+        layer's elements in layer order): right after each group's update,
+        this rank's OWNED published pages of the group go back to the host on
+        a copy stream — the ranks return disjoint pieces, the whole model
+        once per step."""
         buf, ms, lay = self.buffer, self.masters, self.layout
         if self.host_tier:
             raise ConfigError("the layer-group pipeline keeps the state in HBM; a host/SSD-tier "
@@ -392,6 +396,11 @@ class FusedShardedPageStep:
         bc, bc_len = ms._bias(hyper, range(L))
         hc = D.hyper_c(hyper)
         rts = self.__dict__.setdefault("_rts", {})
+        d2h = starts = None
+        if results_to is not None:
+            from .lockfree import _publish_to_host
+            d2h = self.__dict__.setdefault("_d2h", torch.cuda.Stream(self.device))
+            starts = self.__dict__.setdefault("_starts", np.cumsum([0] + lay.numels[:-1]))
         for k, (grp, check, adam) in enumerate(plan):
             first, n = grp[0], len(grp)
             with torch.cuda.stream(rs):
@@ -425,9 +434,13 @@ class FusedShardedPageStep:
                                             D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
                                             self.n, self.mc_p if self.mc_p else None, buf._dt, hc, up_opts,
                                             D.sptr(up)))
+                if d2h is not None:
+                    _publish_to_host(buf, grp, results_to, starts, up, d2h, owned_only=True, pbuf=psel ^ 1)
         mark("rs", rs)
         st.wait_stream(rs)
         st.wait_stream(up)
+        if d2h is not None:
+            st.wait_stream(d2h)
         with torch.cuda.stream(st):
             mark("adam", st)
             self.h_p.barrier(channel=2)                          # published pages landed everywhere

@@ -89,14 +89,27 @@ def main():
         else:
             buf.accumulate_flat(t.to(dev), it)
         gsel = buf._gsel[0]
-        if ingest:
-            step.step_pipelined(hyper, groups, ready=ready)
+        if ingest:   # ... and this rank's owned published pages come back to the host
+            out_host = torch.empty(sum(SIZES), dtype=buf._t16).pin_memory()
+            step.step_pipelined(hyper, groups, ready=ready, results_to=out_host)
         elif groups > 1 and mode != "nccl":
             step.step_pipelined(hyper, groups, reduce_ctas=int(os.environ.get("DP_REDUCE_CTAS", "0")),
                                 update_ctas=int(os.environ.get("DP_UPDATE_CTAS", "0")),
                                 reduce_sms=int(os.environ.get("DP_REDUCE_SMS", "0")))
         else:
             step.step(hyper)
+        if ingest:
+            torch.cuda.synchronize()
+            pub = buf.p16_pool[buf._psel[0]].view(torch.int16).cpu()
+            host16 = out_host.view(torch.int16)
+            base = 0
+            for l, n in enumerate(SIZES):
+                for s_ in lay.segments[l]:
+                    if lay.owned(s_):
+                        off = lay.slot16(s_.page) * lay.E + s_.off
+                        if not torch.equal(host16[base + s_.pos: base + s_.pos + s_.n], pub[off:off + s_.n]):
+                            failures.append(f"it{it} layer{l}: results_to differs from the published page")
+                base += n
         # every owner's reduced (post reduce-scatter) pages, gathered so each
         # rank can run the oracle on the exact captured gradient of ALL pages
         gathered = buf.g16_pool[gsel].clone()
