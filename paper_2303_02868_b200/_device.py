@@ -250,6 +250,24 @@ def check(rc: int) -> None:
     N.check(rc)
 
 
+def pinned_zeros(n: int, dtype=torch.float32) -> torch.Tensor:
+    """Page-locked host tensor of EXACTLY n zeros.  torch's pinned allocator
+    rounds every block up to a power of two (the 13B model's 51.4 GB p32 pool
+    would take 64 GB, and the three state pools 192 GB of a 196 GB box), so
+    large pools are allocated as ordinary host memory and registered with the
+    driver (cudaHostRegister; unregistered when the tensor is freed)."""
+    t = torch.zeros(n, dtype=dtype)
+    nbytes = t.numel() * t.element_size()
+    if nbytes < (1 << 30):
+        return t.pin_memory()
+    cr = torch.cuda.cudart()
+    err = cr.cudaHostRegister(t.data_ptr(), nbytes, 0)
+    if int(err) != 0:
+        raise NativeError(f"cudaHostRegister of {nbytes} bytes failed ({err})")
+    weakref.finalize(t, cr.cudaHostUnregister, t.data_ptr())
+    return t
+
+
 def _parse_cpulist(text: str) -> set[int]:
     cpus = set()
     for part in text.strip().split(","):

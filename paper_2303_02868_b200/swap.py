@@ -57,9 +57,11 @@ class HostMasterState(_Paged):
         self.group_pages = max(1, int(group_pages))
         self.num_groups = -(-lay.P_local // self.group_pages)
         n = lay.elems_state
-        self.host_p = torch.zeros(n, dtype=torch.float32, pin_memory=True)
-        self.host_m = torch.zeros(n, dtype=torch.float32, pin_memory=True)
-        self.host_v = torch.zeros(n, dtype=torch.float32, pin_memory=True)
+        # exact-size page-locked pools (torch's pinned allocator would round
+        # each up to a power of two: 64 GB for C3's 51.4 GB p32 pool)
+        self.host_p = D.pinned_zeros(n)
+        self.host_m = D.pinned_zeros(n)
+        self.host_v = D.pinned_zeros(n)
         for l, p in enumerate(params):
             if p is None:   # caller fills host_p itself (e.g. a bench writing synthetic pages)
                 continue
