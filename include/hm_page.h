@@ -334,6 +334,14 @@ int hm_copy_runs(const void* src, void* dst, const hm_copy_desc* descs,
 int hm_memcpy_runs(const void* src, void* dst, const hm_copy_desc* descs,
                    int64_t n_descs, int kind, void* stream);
 
+/* Page-locked host memory of exactly `bytes` (cudaHostAlloc, portable):
+ * the pinned-host state tier's page pools (the CPU tier of
+ * hiermem/pagemem.py:29-32 holding MasterState, hiermem/lockfree.py:148).
+ * torch's pinned allocator rounds blocks up to powers of two, which does
+ * not fit a 154 GB state in a 196 GB host.  Zero-filled. */
+int hm_host_alloc(int64_t bytes, void** out);
+int hm_host_free(void* ptr);
+
 /* A compute slot of modelled duration when executing an Algorithm-1 schedule
  * (hiermem/scheduler.py:264-403 tasks, durations from hiermem/simengine.py's
  * timing model): one warp spins on %globaltimer for `ns` nanoseconds. */

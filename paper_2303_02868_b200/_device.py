@@ -254,18 +254,19 @@ def pinned_zeros(n: int, dtype=torch.float32) -> torch.Tensor:
     """Page-locked host tensor of EXACTLY n zeros.  torch's pinned allocator
     rounds every block up to a power of two (the 13B model's 51.4 GB p32 pool
     would take 64 GB, and the three state pools 192 GB of a 196 GB box), so
-    large pools are allocated as ordinary host memory and registered with the
-    driver (cudaHostRegister; unregistered when the tensor is freed)."""
-    t = torch.zeros(n, dtype=dtype)
-    nbytes = t.numel() * t.element_size()
+    large pools come from the library's hm_host_alloc (cudaHostAlloc of the
+    exact size), wrapped zero-copy and freed with the tensor."""
+    esz = torch.empty(0, dtype=dtype).element_size()
+    nbytes = n * esz
     if nbytes < (1 << 30):
-        return t.pin_memory()
-    cr = torch.cuda.cudart()
-    err = cr.cudaHostRegister(t.data_ptr(), nbytes, 0)
-    if int(err) != 0:
-        raise NativeError(f"cudaHostRegister of {nbytes} bytes failed ({err})")
-    weakref.finalize(t, cr.cudaHostUnregister, t.data_ptr())
-    return t
+        return torch.zeros(n, dtype=dtype).pin_memory()
+    out = C.c_void_p()
+    check(N.lib().hm_host_alloc(nbytes, C.byref(out)))
+    raw = (C.c_char * nbytes).from_address(out.value)
+    # freed when the last tensor or view over the block goes away (the
+    # storage keeps the buffer object alive)
+    weakref.finalize(raw, N.lib().hm_host_free, C.c_void_p(out.value))
+    return torch.frombuffer(raw, dtype=dtype, count=n)
 
 
 def _parse_cpulist(text: str) -> set[int]:

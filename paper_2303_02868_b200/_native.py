@@ -109,6 +109,8 @@ SIGNATURES = {
     "hm_copy_runs": (_INT, [_P, _P, _P, _I64, _P]),
     "hm_memcpy_runs": (_INT, [_P, _P, _P, _I64, _INT, _P]),
     "hm_spin": (_INT, [_I64, _P]),
+    "hm_host_alloc": (_INT, [_I64, C.POINTER(_P)]),
+    "hm_host_free": (_INT, [_P]),
 }
 
 _lib = None

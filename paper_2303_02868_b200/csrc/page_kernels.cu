@@ -8,6 +8,8 @@
 #include "hm_device.cuh"
 #include "hm_error.h"
 
+#include <cstring>
+
 namespace hm {
 namespace {
 
@@ -581,6 +583,26 @@ int hm_spin(int64_t ns, void* stream) {
   if (ns == 0) return HM_OK;
   hm::spin_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>((uint64_t)ns);
   HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+int hm_host_alloc(int64_t bytes, void** out) {
+  if (bytes <= 0 || !out) return hm_set_error(HM_ERR_INVALID, "hm_host_alloc: bad size %lld", (long long)bytes);
+  *out = nullptr;
+  cudaError_t e = cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    hm_set_alloc_bytes(bytes, 0);
+    return hm_set_error(HM_ERR_ALLOCATION, "hm_host_alloc(%lld bytes): %s", (long long)bytes,
+                        cudaGetErrorString(e));
+  }
+  std::memset(*out, 0, (size_t)bytes);
+  return HM_OK;
+}
+
+int hm_host_free(void* ptr) {
+  if (!ptr) return HM_OK;
+  cudaError_t e = cudaFreeHost(ptr);
+  if (e != cudaSuccess) return hm_set_error(HM_ERR_CUDA, "hm_host_free: %s", cudaGetErrorString(e));
   return HM_OK;
 }
 
