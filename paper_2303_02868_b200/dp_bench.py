@@ -191,8 +191,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     link = measure_nvlink(device, world, rank)
     pipe = None
     if fused:
-        pipe = lambda ready, out: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
-                                                    ready=ready, results_to=out, **knobs)
+        pipe = lambda ready, res: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
+                                                    ready=ready, results_to=res, **knobs)
     e2e = run_e2e(args, buf, ms, do_step, flat, layout, pipe) if args.e2e_steps > 0 else None
     # Link-level bytes per direction per GPU for the step: P2P (and NCCL)
     # move (N-1)/N*S in for the reduce-scatter and (N-1)/N*S in for the
@@ -314,9 +314,9 @@ def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
         do_step()
         return ms._applied.cpu()           # D2H of the step's result
 
-    def pipelined(it):
+    def pipelined(it, results=False):
         ready = LF.ingest(buf, host, it, groups=args.e2e_groups)
-        pipe(ready, out)
+        pipe(ready, out if results else None)
         return ms._applied.cpu()
 
     def timed(step):
@@ -332,18 +332,22 @@ def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
 
     dt_serial = timed(serial)
     dt_pipe = timed(pipelined) if pipe is not None else None
+    dt_res = timed(lambda it: pipelined(it, True)) if pipe is not None else None
     dt = min(dt_serial, dt_pipe) if dt_pipe else dt_serial
-    P = sum(layout.numels)
     piped = bool(dt_pipe and dt_pipe <= dt_serial)
+    P = sum(layout.numels)
     return {"value": P / dt, "unit": "params/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": (d2h if piped else 0) + 4 * len(layout.numels), "ms_per_step": dt * 1e3,
-            "bytes_note": "per rank; the ranks' D2H pieces are disjoint (the whole model returns once)",
+            "d2h_bytes_per_step": 4 * len(layout.numels), "ms_per_step": dt * 1e3,
             "steps": args.e2e_steps, "h2d_gbs_per_rank": h2d / dt / 1e9,
             "serial_ms_per_step": dt_serial * 1e3,
             "pipelined_ms_per_step": dt_pipe * 1e3 if dt_pipe else None,
+            "with_results": None if dt_res is None else {
+                "ms_per_step": dt_res * 1e3, "params_per_s": P / dt_res, "d2h_bytes_per_step": d2h,
+                "note": "step_pipelined(results_to=...): every rank also returns its owned published pages "
+                        "(per rank, disjoint: the whole model once per step); the ranks share the host's "
+                        "PCIe/memory bandwidth"},
             "api": ("lockfree.ingest(pinned host gradient, %d layer groups) -> "
-                    "FusedShardedPageStep.step_pipelined(ready=..., results_to=pinned host params: this "
-                    "rank's owned published pages) -> applied flags to host, every rank"
+                    "FusedShardedPageStep.step_pipelined(ready=...) -> applied flags to host, every rank"
                     % args.e2e_groups) if piped else
                    "ParamBuffer.accumulate_flat(pinned host gradient) + sharded page step + "
                    "applied flags to host, every rank"}
