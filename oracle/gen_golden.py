@@ -19,6 +19,8 @@ Outputs
                            curves for the whole-chain equivalence test
   inventory_param16.json   param16 specs of the reference's tensor_inventory
                            for C1, C2, C3, C5
+  tracer_inventory.json    the names a TimingModel table must cover for the
+                           traced test shape
 """
 from __future__ import annotations
 
@@ -162,6 +164,17 @@ def inventories():
         json.dump(out, fh)
 
 
+def tracer_inventory():
+    """Every tensor name the reference's build_trace needs a TimingModel table
+    entry for (hiermem/tracer.py:102-107, 138-170: all but optim32), for the
+    shape tests/test_gpu_tracing.py traces (seq 128, d 256, ffn 1024, 4 heads,
+    2 layers)."""
+    cfg = footprint.TransformerConfig(1, 128, 256, 1024, 2, 4)
+    names = [s.name for s in footprint.tensor_inventory(cfg) if s.kind != "optim32"]
+    with open(GOLDEN / "tracer_inventory.json", "w") as fh:
+        json.dump({"shape": [1, 128, 256, 1024, 2, 4], "names": names}, fh)
+
+
 def toy_sync():
     cfg = lockfree.ToyTrainConfig(num_layers=3, dim=16, batch_size=32, seed=5, noise_std=1.0)
     ref = lockfree.reference_train(cfg, 25)
@@ -228,6 +241,7 @@ if __name__ == "__main__":
     pagetable_random()
     pagetable_configs()
     inventories()
+    tracer_inventory()
     toy_sync()
     schedules()
     print("golden fixtures written to", GOLDEN)

@@ -19,6 +19,15 @@ def test_timing_table_covers_inventory(cuda):
     assert names <= set(table)
     for name, (cpu, gpu) in table.items():
         assert cpu >= 0.0 and gpu >= 0.0, name
+    # every name the reference's build_trace looks up (all but optim32,
+    # hiermem/tracer.py:102-107) — pinned by a golden of the reference
+    # inventory; tests/test_tracer_presets.py feeds tables of this format to
+    # the reference itself
+    import json
+    from conftest import GOLDEN
+    need = json.loads((GOLDEN / "tracer_inventory.json").read_text())["names"]
+    missing = [n for n in need if n not in table]
+    assert not missing, missing[:5]
     rows = d["_measured_rows"]
     assert set(rows) == set(ROWS)
     assert rows["ffn.linear_in"]["forward_s"] > 0
