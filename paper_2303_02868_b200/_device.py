@@ -3,6 +3,7 @@ tensors into raw pointers for the C-ABI, caches descriptor uploads, and
 holds the exact bias-correction tables.  No compute happens here."""
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import weakref
 from collections import OrderedDict
@@ -38,8 +39,28 @@ def addr(x) -> int:
     return x if isinstance(x, int) else ptr(x)
 
 
+_STREAMS: dict = {}
+
+
 def cur_stream(device, stream=None):
-    return stream if stream is not None else torch.cuda.current_stream(device)
+    """``stream`` or the device's current stream.  Same object as
+    torch.cuda.current_stream(device), without its per-call device-index
+    resolution (the three-call path asks ~7 times per layer)."""
+    if stream is not None:
+        return stream
+    sid, didx, dtype = torch._C._cuda_getCurrentStream(device.index)
+    s = _STREAMS.get((sid, didx))
+    if s is None:
+        s = _STREAMS[(sid, didx)] = torch.cuda.Stream(stream_id=sid, device_index=didx, device_type=dtype)
+    return s
+
+
+def on(stream):
+    """``torch.cuda.stream(stream)``, or a no-op when it already is the
+    current stream (allocations then land on it either way)."""
+    if torch._C._cuda_getCurrentStream(stream.device_index)[0] == stream.stream_id:
+        return contextlib.nullcontext()
+    return torch.cuda.stream(stream)
 
 
 def sptr(stream) -> C.c_void_p:
@@ -49,7 +70,9 @@ def sptr(stream) -> C.c_void_p:
 class DescCache:
     """Device copies of host descriptor arrays.  Static plans are keyed by the
     identity of the (cached, immortal) numpy array; per-launch tables by their
-    bytes in a small LRU, so steady-state sweeps upload nothing.
+    bytes in an LRU sized for every layer's rows of both page buffers (the
+    three-call path looks up a few hundred small tables per step), so steady
+    state uploads nothing.
 
     Uploads are allocated on the caller's current stream.  A table used by a
     launch on another stream names that stream (``table(arr, stream)``):
@@ -57,7 +80,7 @@ class DescCache:
     that used it, so the caching allocator cannot hand the block to a new
     upload while a queued kernel may still read it."""
 
-    def __init__(self, device, lru: int = 64):
+    def __init__(self, device, lru: int = 8192):
         self.device = device
         self._static: dict[int, tuple[np.ndarray, torch.Tensor]] = {}
         self._lru: OrderedDict[bytes, tuple[torch.Tensor, set]] = OrderedDict()

@@ -327,7 +327,7 @@ class Applied:
 
     def __bool__(self) -> bool:
         if self._v is None:
-            with torch.cuda.stream(self._stream):
+            with D.on(self._stream):
                 self._v = bool(self._t.item())
         return self._v
 
@@ -353,7 +353,7 @@ def apply_update(p32, m32, v32, grad, hyper: AdamHyper, step: int, *, stream=Non
     eng = _Engine.of(device)
     st = D.cur_stream(device, stream)
     shape = _shape(p32)
-    with torch.cuda.stream(st):
+    with D.on(st):
         p = D.to_device_flat(p32, device).to(torch.float32).clone()
         m = D.to_device_flat(m32, device).to(torch.float32).clone()
         v = D.to_device_flat(v32, device).to(torch.float32).clone()
@@ -363,7 +363,7 @@ def apply_update(p32, m32, v32, grad, hyper: AdamHyper, step: int, *, stream=Non
         raise ProtocolError(f"apply_update: size mismatch p={n} m={m.numel()} v={v.numel()} g={g.numel()}")
     if n == 0:
         return p32, m32, v32, True
-    with torch.cuda.stream(st):
+    with D.on(st):
         bc = torch.tensor([float(np.float32(1.0 - hyper.beta1 ** step)),
                            float(np.float32(1.0 - hyper.beta2 ** step))], dtype=torch.float32, device=device)
         flag = torch.zeros(1, dtype=torch.int32, device=device)
@@ -374,7 +374,7 @@ def apply_update(p32, m32, v32, grad, hyper: AdamHyper, step: int, *, stream=Non
     adam_launch(eng, D.contiguous_adam_chunks(n), _group_rows([(0, 0, 0, 0)]), g, D.DT_OF_TORCH[g.dtype],
                 p, m, v, None, 0, hyper, bc, 1, int(step), None, applied, flag, None, True, st,
                 static_chunks=False)
-    with torch.cuda.stream(st):
+    with D.on(st):
         if not bool(applied.item()):
             return p32, m32, v32, False
         if numpy_io:
@@ -473,7 +473,7 @@ class MasterState(_Paged):
         self.tier = tier
         lay = self.layout
         st = self._stream()
-        with torch.cuda.stream(st):
+        with D.on(st):
             self.p32_pool = torch.zeros(lay.elems_state, dtype=torch.float32, device=self.device)
             self.m32_pool = torch.zeros_like(self.p32_pool)
             self.v32_pool = torch.zeros_like(self.p32_pool)
@@ -514,7 +514,7 @@ class MasterState(_Paged):
     def _pack_p32(self, layer, value, stream=None):
         self._prepub[layer] = None
         st = self._stream(stream)
-        with torch.cuda.stream(st):
+        with D.on(st):
             src = D.to_device_flat(value, self.device)
             if src.dtype != torch.float32:
                 src = src.float()
@@ -523,7 +523,7 @@ class MasterState(_Paged):
 
     def _unpack(self, pool, layer, stream=None):
         st = self._stream(stream)
-        with torch.cuda.stream(st):
+        with D.on(st):
             # world 1: every element is written by the unpack; sharded: the
             # pages other ranks own read as zeros
             alloc = torch.empty if self.layout.world_size == 1 else torch.zeros
@@ -562,20 +562,20 @@ class MasterState(_Paged):
                     and buf._gsel[layer] != h.gbuf and self._same_pages(buf.layout)
                     and buf.device == self.device):
                 return self._update_from_pages(buf, h.gbuf, layer, hyper, st)
-        with torch.cuda.stream(st):
+        with D.on(st):
             g = D.to_device_flat(grad, self.device)
         n = self.layout.numels[layer]
         if g.numel() != n:
             raise ProtocolError(f"gradient has {g.numel()} elements, layer {layer} has {n}")
         eng = self._eng
         flag = eng.scratch(st).flag
-        with torch.cuda.stream(st):
+        with D.on(st):
             flag.zero_()
         cc = D.contiguous_chunks_cached(n)
         D.check(N.lib().hm_reduce_stats(D.ptr(g), D.DT_OF_TORCH[g.dtype], D.ptr(eng.desc.static(cc)),
                                          len(cc), D.ptr(flag), None, None, D.sptr(st)))
         bc, bc_len = self._bias(hyper, [layer])
-        with torch.cuda.stream(st):
+        with D.on(st):
             out = torch.empty(1, dtype=torch.int32, device=self.device)
         adam_launch(eng, self.layout.adam_chunks([layer], "tensor"), _group_rows([(0, 0, 0, 0)]),
                     g, D.DT_OF_TORCH[g.dtype], self.p32_pool, self.m32_pool, self.v32_pool, None, 0,
@@ -587,7 +587,7 @@ class MasterState(_Paged):
         nxt = buf._psel[layer] ^ 1
         fidx = gbuf * L + layer
         bc, bc_len = self._bias(hyper, [layer])
-        with torch.cuda.stream(st):
+        with D.on(st):
             out = torch.empty(1, dtype=torch.int32, device=self.device)
         # group 0 of the launch = this layer: steps[] is addressed at the
         # layer's counter, applied[] is the per-call result word
@@ -603,7 +603,7 @@ class MasterState(_Paged):
 
     def _applied_result(self, out: torch.Tensor, st):
         if self._numpy:
-            with torch.cuda.stream(st):
+            with D.on(st):
                 return bool(out.item())
         return Applied(out, st)
 
@@ -641,7 +641,7 @@ class ParamBuffer(_Paged):
         self._dt = N.DTYPE_CODES[dtype]
         L, lay = self.num_layers, self.layout
         st = self._stream()
-        with torch.cuda.stream(st):
+        with D.on(st):
             if pool_alloc is None:
                 self.g16_pool = torch.zeros(2, lay.elems16, dtype=self._t16, device=self.device)
                 self.p16_pool = torch.zeros(2, lay.elems16, dtype=self._t16, device=self.device)
@@ -669,7 +669,7 @@ class ParamBuffer(_Paged):
         if ledger:
             self.ledger._resolver = self._ledger_flush
         for l, p in enumerate(initial_params):
-            with torch.cuda.stream(st):
+            with D.on(st):
                 src = D.to_device_flat(p, self.device)
                 if src.dtype != torch.float32:
                     src = src.float()
@@ -767,7 +767,7 @@ class ParamBuffer(_Paged):
 
     def _unpack16(self, pool, layer, readonly=False, stream=None, raw=False):
         st = self._stream(stream)
-        with torch.cuda.stream(st):
+        with D.on(st):
             out = torch.empty(self.layout.numels[layer], dtype=self._t16, device=self.device)
         self._cast(pool, self._dt, out, self._dt, self.layout.seg_chunks(layer, "16", reverse=True), st)
         return out if raw else self._out(out, layer, readonly)
@@ -827,7 +827,7 @@ class ParamBuffer(_Paged):
             raise ProtocolError(f"gradient shape {_shape(msg.payload)} != buffer shape "
                                 f"{self._shapes[layer]} for layer {layer}")
         st = self._stream(stream)
-        with torch.cuda.stream(st):
+        with D.on(st):
             src = D.to_device_flat(msg.payload, self.device)
         f = self._gsel[layer] * self.num_layers + layer
         self._k3(src, D.DT_OF_TORCH[src.dtype], self._acc_plan([layer], None),
@@ -839,7 +839,7 @@ class ParamBuffer(_Paged):
         flags and ledger entries as one ``accumulate`` per layer."""
         L, lay = self.num_layers, self.layout
         st = self._stream(stream)
-        with torch.cuda.stream(st):
+        with D.on(st):
             src = D.to_device_flat(flat, self.device)
         if src.numel() != sum(lay.numels):
             raise ProtocolError(f"flat gradient has {src.numel()} elements, layers hold "
@@ -877,7 +877,7 @@ class ParamBuffer(_Paged):
             return None
         st = self._stream(stream)
         buf, count, newest = self._hand_over(layer)
-        with torch.cuda.stream(st):
+        with D.on(st):
             g = torch.empty(self.layout.numels[layer], dtype=torch.float32, device=self.device)
         self._cast(self.g16_pool[buf], self._dt, g, N.DT_F32,
                    self.layout.seg_chunks(layer, "16", reverse=True), st)
@@ -922,7 +922,7 @@ class ParamBuffer(_Paged):
         if (tag is not None and pre is not None and tag[0]() is self and tag[1] is pre[0]
                 and tag[2] == layer and p32._version == tag[3] and pre[1] == self._psel[layer] ^ 1):
             return self._published(layer, applied_iter)   # update_layer already cast these values
-        with torch.cuda.stream(st):
+        with D.on(st):
             src = D.to_device_flat(p32, self.device)
             if src.dtype != torch.float32:
                 src = src.float()
