@@ -40,10 +40,17 @@ def main():
     mode = os.environ.get("DP_MODE", "nccl")
     buf = LF.ParamBuffer([torch.from_numpy(p) for p in params], dtype=dtype, page_bytes=PAGE,
                          device=dev, layout=lay, pool_alloc=None if mode == "nccl" else symmetric_alloc)
-    if os.environ.get("DP_HOST", "0") == "1":   # fp32 state in pinned host memory, owned pages only
+    host_tier = os.environ.get("DP_HOST", "0")
+    if host_tier == "1":   # fp32 state in pinned host memory, owned pages only
         from paper_2303_02868_b200.swap import HostMasterState
         ms = HostMasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay,
                              group_pages=2, world_size=world, rank=rank)
+    elif host_tier == "ssd":   # fp32 state in a per-rank file (owned pages only)
+        import tempfile
+        from paper_2303_02868_b200.ssd import SSDMasterState
+        path = os.path.join(tempfile.gettempdir(), f"hm_dp_state_{os.getpid()}_{rank}.bin")
+        ms = SSDMasterState([torch.from_numpy(p) for p in params], path, page_bytes=PAGE, device=dev,
+                            layout=lay, group_pages=2, world_size=world, rank=rank)
     else:
         ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay)
     step = ShardedPageStep(buf, ms) if mode == "nccl" else FusedShardedPageStep(buf, ms, mode=mode)
@@ -176,6 +183,9 @@ def main():
             if lay.owned(s) and not np.array_equal(mp[s.pos:s.pos + s.n].view(np.uint32),
                                                    om.p32[l][s.pos:s.pos + s.n].view(np.uint32)):
                 failures.append(f"layer{l} page{s.page}: owned p32 differs")
+    if host_tier == "ssd":
+        ms.close()
+        os.unlink(path)
     ok = torch.tensor([0 if failures else 1], device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if stats:

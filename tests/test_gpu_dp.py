@@ -28,7 +28,8 @@ CASES = [
     (2, "bf16", "p2p", 4, "green32"),  # reduce and update in two green contexts (SM partitions)
     (2, "bf16", "p2p", 1, "wide8"), (2, "fp16", "p2p", 3, "wide8"),  # 8-peer reduce kernel
     (2, "bf16", "p2p", 1, "ld128"),   # the 16 B-load reduce (256-bit loads are the default)
-    (2, "bf16", "p2p", 1, "host"), (3, "fp16", "p2p", 1, "host")]   # fp32 state on the pinned-host tier
+    (2, "bf16", "p2p", 1, "host"), (3, "fp16", "p2p", 1, "host"),   # fp32 state on the pinned-host tier
+    (2, "bf16", "p2p", 1, "ssd")]    # fp32 state in a file per rank (SSD tier)
 SMOKE2 = [CASES[1], CASES[3], CASES[6], CASES[12], CASES[17]]
 
 
@@ -54,8 +55,8 @@ def test_dp_step_two_ranks(bucket, dtype, mode, groups, ctas):
 
 def _run(world, bucket, dtype, mode, groups, ctas):
     agp, upd, ingest, green, width, ld256, host = 0, 0, 0, 0, 0, 0, 0
-    if ctas == "host":
-        host, ctas = 1, 0
+    if ctas in ("host", "ssd"):
+        host, ctas = (1 if ctas == "host" else "ssd"), 0
     elif ctas == "ld128":
         ld256, ctas = 1, 0
     elif ctas == "wide8":   # the 8-wide reduce instantiation (what N=8 runs), with a persistent grid when pipelined
