@@ -610,7 +610,7 @@ class MasterState(_Paged):
 
 # ---- ParamBuffer (hiermem/lockfree.py:174-263) ---------------------------------------
 
-_RING_ROWS = 1024
+_RING_ROWS = 4096   # ledger rows between host resolutions (one per accumulate launch or take)
 
 
 class ParamBuffer(_Paged):
