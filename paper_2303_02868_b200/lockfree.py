@@ -594,8 +594,10 @@ class MasterState(_Paged):
         adam_launch(self._eng, self.layout.adam_chunks([layer], "pool"),
                     _group_rows([(gbuf * span, nxt * span, 0, fidx)]), buf.g16_pool, buf._dt,
                     self.p32_pool, self.m32_pool, self.v32_pool, buf.p16_pool, buf._dt, hyper, bc, bc_len,
-                    0, D.ptr(self._steps) + 4 * layer, out, buf._flags, buf._sumsq, True, st)
-        buf._dirty.discard(fidx)
+                    0, D.ptr(self._steps) + 4 * layer, out, buf._flags, buf._sumsq, False, st)
+        # the flag is read, not consumed: a second update_layer of the same
+        # tensor must see the same verdict (the reference re-checks, :133);
+        # the slot stays marked for a reset before its next first message
         token = object()
         buf._prepub[layer] = (token, nxt)
         self._prepub[layer] = (weakref.ref(buf), token)

@@ -110,3 +110,24 @@ def test_ingest_sweep_returns_published_pages(cuda):
             assert torch.equal(host_out[pos:pos + n].view(torch.int16),
                                buf.layer_view(l).cpu().view(torch.int16)), (it, l)
             pos += n
+
+
+def test_three_call_fast_path_rejects_every_time(cuda):
+    """update_layer on a taken tensor re-uses the reject flag the accumulate
+    computed; calling it twice with a NaN gradient must reject twice, like
+    the reference's apply_update (hiermem/lockfree.py:133-134)."""
+    params = [torch.zeros(4096, device="cuda"), torch.zeros(100, device="cuda")]
+    buf, ms = LF.ParamBuffer(params, page_bytes=PAGE), LF.MasterState(params, page_bytes=PAGE)
+    g = torch.ones(4096, dtype=torch.float16, device="cuda")
+    g[17] = float("nan")
+    buf.accumulate(LF.GradMessage(0, g, 0))
+    gr, _, _ = buf.take(0)
+    assert not bool(ms.update_layer(0, gr, LF.AdamHyper()))
+    assert not bool(ms.update_layer(0, gr, LF.AdamHyper()))
+    assert ms.steps == [0, 0]
+    # the slot starts clean for the next first message
+    buf.accumulate(LF.GradMessage(0, torch.ones(4096, dtype=torch.float16, device="cuda"), 1))
+    gr, _, _ = buf.take(0)
+    buf.accumulate(LF.GradMessage(0, torch.ones(4096, dtype=torch.float16, device="cuda"), 2))
+    assert bool(ms.update_layer(0, gr, LF.AdamHyper()))
+    assert ms.steps == [1, 0]
