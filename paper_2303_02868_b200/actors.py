@@ -11,7 +11,8 @@ publish -> store).  Here the actors are streams:
   page buffer, then ``accumulate_flat`` of the gradient into the active
   gradient page buffer (the buffering actor's accumulate, K3);
 * update stream   (updating actor): ``sweep`` — or ``swap_sweep`` when the
-  fp32 state lives in pinned host memory — takes the buffer, updates and
+  fp32 state lives in pinned host memory, or the data-parallel page step
+  (reduce-scatter -> update -> all-gather) — takes the buffer, updates and
   publishes into the inactive parameter buffer (K2 + K8);
 * events replace mailboxes: the update of iteration k waits for the
   accumulate of k; with ``delay=1`` the compute of k+1 reads the parameters
@@ -54,7 +55,7 @@ class RunReport:
 
 class LockFreeRunner:
     def __init__(self, buffer: ParamBuffer, masters, hyper, *, delay: int = 1,
-                 compute_stream=None, update_stream=None):
+                 compute_stream=None, update_stream=None, update=None):
         if delay not in (0, 1):
             raise ConfigError("delay must be 0 (synchronous) or 1 (lock-free, staleness <= 1)")
         self.buffer, self.masters, self.hyper, self.delay = buffer, masters, hyper, delay
@@ -62,7 +63,10 @@ class LockFreeRunner:
         self.cs = compute_stream or torch.cuda.Stream(dev)
         self.us = update_stream or torch.cuda.Stream(dev)
         from .swap import HostMasterState, swap_sweep
-        self._sweep = swap_sweep if isinstance(masters, HostMasterState) else sweep
+        # the updating actor's step: the fused sweep, the swap sweep for a
+        # host-tier state, or a caller's (e.g. the data-parallel page step,
+        # ``lambda buf, ms, hyper, stream: dp.step(hyper, stream=stream)``)
+        self._sweep = update or (swap_sweep if isinstance(masters, HostMasterState) else sweep)
         self._pub: list[tuple[torch.cuda.Event, int, int]] = []   # (event, psel, version)
         self._it = 0                  # global iteration counter across run() calls
         self._psel0 = buffer._psel[0]

@@ -242,8 +242,13 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
                 (", all ranks at once, slowest rank" if world > 1 else ""),
                 "bytes_per_param": 24, "per": "rank (its owned pages over its own PCIe link)", "pcie": pcie}
     lockfree = None
-    if world == 1 and args.state_tier == "host" and args.c3_lockfree_iters > 0:
-        lockfree = _lockfree(args, buf, hm, hyper, grads, P, device)
+    if args.state_tier == "host" and args.c3_lockfree_iters > 0:
+        upd = (lambda b, m, h, stream: dp.step(h, stream=stream)) if world > 1 else None
+        lockfree = _lockfree(args, buf, hm, hyper, grads, P, device, update=upd)
+        if world > 1:
+            for k in ("sync_iter_ms", "lockfree_iter_ms"):
+                lockfree[k] = _max_over_ranks(lockfree[k])
+            lockfree["speedup"] = lockfree["sync_iter_ms"] / lockfree["lockfree_iter_ms"]
     line = {
         "metric": metric, "value": P / (ms_step / 1e3), "unit": "params/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -280,10 +285,11 @@ def _min_over_ranks(x: float) -> float:
     return float(t.item())
 
 
-def _lockfree(args, buf, hm, hyper, grads, P, device):
+def _lockfree(args, buf, hm, hyper, grads, P, device, update=None):
     """C3's "lock-free delayed update" (Algorithm 2) on the
-    same pools: actors.LockFreeRunner with the host-tier sweep as the
-    updating actor and, as the GPU actor, the slice's forward+backward
+    same pools: actors.LockFreeRunner with the host-tier sweep (or, at N > 1,
+    the DP page step over the sharded host tier) as the updating actor and,
+    as the GPU actor, the slice's forward+backward
     modelled as a spin of 6 x params x tokens / (measured bf16 peak x MFU) —
     the update path is the product here, not the model.  delay=0 is the
     synchronous loop (update, then the next compute); delay=1 overlaps the
@@ -303,9 +309,10 @@ def _lockfree(args, buf, hm, hyper, grads, P, device):
         return zero, grads
 
     out = {"gpu_actor": f"spin of 6 x {P} params x {tokens} tokens / ({bf16} TF/s x MFU {mfu})",
-           "compute_ms": tc_ms, "iters": args.c3_lockfree_iters}
+           "compute_ms": tc_ms, "iters": args.c3_lockfree_iters,
+           "updating_actor": "swap sweep" if update is None else "DP page step with the host-tier state"}
     for delay, name in ((0, "sync"), (1, "lockfree")):
-        runner = LockFreeRunner(buf, hm, hyper, delay=delay)
+        runner = LockFreeRunner(buf, hm, hyper, delay=delay, update=update)
         runner.run(1, grads_fn, mode=name)                     # warm-up iteration
         rep = runner.run(args.c3_lockfree_iters, grads_fn, mode=name)
         out[f"{name}_iter_ms"] = rep.iter_ms

@@ -82,3 +82,21 @@ def _run(world, bucket, dtype, mode, groups, ctas):
            "--master-addr=127.0.0.1", "--master-port=29611", str(ROOT / "tests" / "dp_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
+
+
+@pytest.mark.parametrize("delay", [0, 1])
+def test_lockfree_runner_with_dp_step(delay):
+    """Algorithm 2 on N GPUs: the lock-free runner's updating actor is the DP
+    page step over the sharded pinned-host state (tests/dp_lockfree_worker.py)."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = _world(n)
+    env = dict(os.environ, DP_DELAY=str(delay))
+    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+    ids = visible.split(",") if visible else [str(i) for i in range(n)]
+    env["CUDA_VISIBLE_DEVICES"] = ",".join(ids[:world])
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29612", str(ROOT / "tests" / "dp_lockfree_worker.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
