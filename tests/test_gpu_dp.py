@@ -100,3 +100,21 @@ def test_lockfree_runner_with_dp_step(delay):
            "--master-addr=127.0.0.1", "--master-port=29612", str(ROOT / "tests" / "dp_lockfree_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
+
+
+@pytest.mark.parametrize("pipe", [0, 1])
+def test_dp_step_full_c2_sampled(pipe):
+    """The fused DP step at the size bench.py measures (C2, 4 MiB pages),
+    sampled pages bit-exact (tests/dp_fullsize_worker.py)."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = _world(n)
+    env = dict(os.environ, DP_PIPE=str(pipe))
+    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+    ids = visible.split(",") if visible else [str(i) for i in range(n)]
+    env["CUDA_VISIBLE_DEVICES"] = ",".join(ids[:world])
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29613", str(ROOT / "tests" / "dp_fullsize_worker.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
