@@ -401,20 +401,32 @@ class FusedShardedPageStep:
             from .lockfree import _publish_to_host
             d2h = self.__dict__.setdefault("_d2h", torch.cuda.Stream(self.device))
             starts = self.__dict__.setdefault("_starts", np.cumsum([0] + lay.numels[:-1]))
+        gmarks = []
+
+        def gmark(s):
+            if timings is None:
+                return None
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            return e
+
         for k, (grp, check, adam) in enumerate(plan):
             first, n = grp[0], len(grp)
             with torch.cuda.stream(rs):
                 if ready is not None:
                     rs.wait_event(ready[k])
                     self.h_g.barrier(channel=0)                  # group k landed on every rank
+                r0 = gmark(rs)
                 D.check(lib.hm_dp_reduce_check(gp, self.n, mc, D.ptr(buf.g16_pool[gsel]), buf._dt,
                                                D.ptr(eng.desc.static(check)), len(check),
                                                D.ptr(self.flags_local), None, rs_opts, D.sptr(rs)))
+                r1 = gmark(rs)
                 self.h_f.barrier(channel=1)                      # group k's flags visible everywhere
                 done = torch.cuda.Event()
                 done.record(rs)
             up.wait_event(done)
             with torch.cuda.stream(up):
+                u0 = gmark(up)
                 D.check(lib.hm_dp_flags_merge(self._arr([p + 4 * first for p in self.f_ptrs]), None,
                                               self.n, n, D.ptr(self.flags) + 4 * first, None, D.sptr(up)))
                 rows = t.groups[first:first + n].copy()
@@ -434,6 +446,7 @@ class FusedShardedPageStep:
                                             D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), self._arr(self.p_ptrs),
                                             self.n, self.mc_p if self.mc_p else None, buf._dt, hc, up_opts,
                                             D.sptr(up)))
+                gmarks.append((r0, r1, u0, gmark(up)))
                 if d2h is not None:
                     _publish_to_host(buf, grp, results_to, starts, up, d2h, owned_only=True, pbuf=psel ^ 1)
         mark("rs", rs)
@@ -451,6 +464,7 @@ class FusedShardedPageStep:
         t.finish(consumed_flags=False)
         if timings is not None:
             timings["_marks"] = marks
+            timings["_groups"] = gmarks     # per group: reduce start/end, update start/end
         return list(range(L))
 
     def step(self, hyper, *, stream=None, ag_publish: int = -1, reduce_wide: int = -1,
