@@ -266,7 +266,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks):
                            "page-Adam with all-gather epilogue -> D2H"},
         "roofline": roof,
         "clocks": clk.summary(),
-        "gpu_launches": args.steps * (1 + hm.num_groups + (4 if world > 1 else 0)),
+        # prologue + one page-Adam per page group (+ reduce-scatter and flag merge at N > 1)
+        "gpu_launches": args.steps * (1 + hm.num_groups + (2 if world > 1 else 0)),
     }
     if lockfree:
         line["lockfree"] = lockfree
