@@ -525,7 +525,7 @@ def main():
                          "step is NVLink-bound — profiles/r1_dp_c2.md)")
     ap.add_argument("--ag-publish", type=int, default=0, choices=[0, 1, 2],
                     help="fused DP all-gather epilogue: 0 per-thread peer stores, 1 per-CTA bulk "
-                         "copies (cp.async.bulk), 2 bulk + wait for remote completion")
+                         "copies (cp.async.bulk, waiting for the remote writes); 2 = 1")
     ap.add_argument("--dp-reduce-wide", type=int, default=1, choices=[0, 1],
                     help="fused DP reduce with 256-bit peer loads (hm_set_dp_reduce_wide; 0 = 16 B loads)")
     ap.add_argument("--dp-reduce-sms", type=int, default=0,

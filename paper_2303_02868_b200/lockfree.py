@@ -698,9 +698,6 @@ class ParamBuffer(_Paged):
         torch.cuda.synchronize(self.device)   # rows are zero before any stream reuses them
         self._ring_pos = 0
 
-    def _slots_table(self, slots) -> torch.Tensor:
-        return self._eng.desc.table(np.asarray(slots, dtype=np.uint32))
-
     def _reset_dirty(self, slots, stream) -> None:
         """Reset the flag / norm / ledger sum of slots about to take a first
         message, if a hand-over left them unconsumed (one launch)."""

@@ -179,7 +179,7 @@ def test_sweep_matches_oracle_bit_exact(cuda, dtype):
     sizes = _layer_sizes()
     rng = np.random.default_rng(5)
     params = [rng.normal(0, 0.02, n).astype(np.float32) for n in sizes]
-    buf = LF.ParamBuffer(params, dtype=dtype, page_bytes=64 * 1024, ledger=True)
+    buf = LF.ParamBuffer(params, dtype=dtype, page_bytes=64 * 1024)   # the ledger is on by default
     ms = LF.MasterState(params, page_bytes=64 * 1024)
     om = O.OracleMasters(params)
     hyper = LF.AdamHyper(lr=1e-3)
