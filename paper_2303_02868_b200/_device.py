@@ -40,6 +40,9 @@ def addr(x) -> int:
 
 
 _STREAMS: dict = {}
+# torch's own binding behind torch.cuda.current_stream (private: fall back to
+# the public call if a torch build does not have it)
+_GET_CURRENT = getattr(torch._C, "_cuda_getCurrentStream", None)
 
 
 def cur_stream(device, stream=None):
@@ -48,7 +51,9 @@ def cur_stream(device, stream=None):
     resolution (the three-call path asks ~7 times per layer)."""
     if stream is not None:
         return stream
-    sid, didx, dtype = torch._C._cuda_getCurrentStream(device.index)
+    if _GET_CURRENT is None:
+        return torch.cuda.current_stream(device)
+    sid, didx, dtype = _GET_CURRENT(device.index)
     s = _STREAMS.get((sid, didx))
     if s is None:
         s = _STREAMS[(sid, didx)] = torch.cuda.Stream(stream_id=sid, device_index=didx, device_type=dtype)
@@ -58,7 +63,7 @@ def cur_stream(device, stream=None):
 def on(stream):
     """``torch.cuda.stream(stream)``, or a no-op when it already is the
     current stream (allocations then land on it either way)."""
-    if torch._C._cuda_getCurrentStream(stream.device_index)[0] == stream.stream_id:
+    if _GET_CURRENT is not None and _GET_CURRENT(stream.device_index)[0] == stream.stream_id:
         return contextlib.nullcontext()
     return torch.cuda.stream(stream)
 
