@@ -64,7 +64,8 @@ def main():
     from paper_2303_02868_b200.sharding import PageCollectives
     coll = PageCollectives(lay)
     om = O.OracleMasters(params)
-    hyper = LF.AdamHyper(lr=1e-3)
+    clip = float(os.environ.get("DP_CLIP", "0"))   # global grad-norm clip over every rank's layers
+    hyper = LF.AdamHyper(lr=1e-3, max_norm=clip)
     failures = []
     stats = {}
     if mode != "nccl":
@@ -123,6 +124,7 @@ def main():
         coll.all_gather(gathered)
         torch.cuda.synchronize()
         gpool = gathered.view(torch.int16).cpu().numpy().view(np.uint16 if dtype == "bf16" else np.float16)
+        caps = []
         for l, n in enumerate(SIZES):
             if mode == "nccl":   # NCCL ring: each hop adds into a 16-bit buffer
                 red = per_rank[0][l]
@@ -167,8 +169,24 @@ def main():
                     if np.isfinite(gf).sum() != fin.sum():
                         failures.append(f"it{it} layer{l}: non-finite pattern differs")
                 captured[s.pos:s.pos + s.n] = got
-            # oracle Adam on the captured reduced gradient
-            om.update_layer(l, O.from16(captured, dtype), lr=1e-3)
+            caps.append(captured)
+        # oracle Adam on the captured reduced gradient (clip: the global norm
+        # of the layers that will be applied, the device's coefficient rule)
+        gscale = None
+        if clip > 0:
+            tot = 0.0
+            for c in caps:
+                g = O.from16(c, dtype).astype(np.float64)
+                if np.isfinite(g).all():
+                    tot += float(np.sum(g * g))
+            norm = np.sqrt(tot)
+            coef = clip / (norm + 1e-6) if norm > clip else 1.0
+            gscale = np.float32(np.float32(1.0) * np.float32(coef))
+        for l, c in enumerate(caps):
+            g = O.from16(c, dtype)
+            if gscale is not None:
+                g = (g * gscale).astype(np.float32)
+            om.update_layer(l, g, lr=1e-3)
     steps = ms.steps
     if steps != om.steps:
         failures.append(f"steps {steps} != oracle {om.steps}")
@@ -178,6 +196,14 @@ def main():
         want16 = O.to16(om.p32[l], dtype).view(np.uint16)
         for s in lay.segments[l]:
             off = lay.slot16(s.page) * lay.E + s.off
+            if clip > 0:   # the device's f32-partial norm may move the coefficient by a last bit
+                d16 = np.abs(p16[off:off + s.n].astype(np.int32) - want16[s.pos:s.pos + s.n].astype(np.int32))
+                if d16.max(initial=0) > 1:
+                    failures.append(f"layer{l} page{s.page}: all-gathered p16 off by {d16.max()} ulp")
+                if lay.owned(s) and not np.allclose(mp[s.pos:s.pos + s.n], om.p32[l][s.pos:s.pos + s.n],
+                                                    rtol=1e-6, atol=1e-12):
+                    failures.append(f"layer{l} page{s.page}: owned p32 beyond 1e-6 relative")
+                continue
             if not np.array_equal(p16[off:off + s.n], want16[s.pos:s.pos + s.n]):
                 failures.append(f"layer{l} page{s.page}: all-gathered p16 differs")
             if lay.owned(s) and not np.array_equal(mp[s.pos:s.pos + s.n].view(np.uint32),

@@ -29,7 +29,8 @@ CASES = [
     (2, "bf16", "p2p", 1, "wide8"), (2, "fp16", "p2p", 3, "wide8"),  # 8-peer reduce kernel
     (2, "bf16", "p2p", 1, "ld128"),   # the 16 B-load reduce (256-bit loads are the default)
     (2, "bf16", "p2p", 1, "host"), (3, "fp16", "p2p", 1, "host"),   # fp32 state on the pinned-host tier
-    (2, "bf16", "p2p", 1, "ssd")]    # fp32 state in a file per rank (SSD tier)
+    (2, "bf16", "p2p", 1, "ssd"),    # fp32 state in a file per rank (SSD tier)
+    (2, "bf16", "p2p", 1, "clip"), (2, "fp16", "nccl", 1, "clip")]   # global grad-norm clip over all ranks
 SMOKE2 = [CASES[1], CASES[3], CASES[6], CASES[12], CASES[17]]
 
 
@@ -55,7 +56,10 @@ def test_dp_step_two_ranks(bucket, dtype, mode, groups, ctas):
 
 def _run(world, bucket, dtype, mode, groups, ctas):
     agp, upd, ingest, green, width, ld256, host = 0, 0, 0, 0, 0, 0, 0
-    if ctas in ("host", "ssd"):
+    clip = 0.0
+    if ctas == "clip":
+        clip, ctas = 1.0, 0
+    elif ctas in ("host", "ssd"):
         host, ctas = (1 if ctas == "host" else "ssd"), 0
     elif ctas == "ld128":
         ld256, ctas = 1, 0
@@ -72,7 +76,8 @@ def _run(world, bucket, dtype, mode, groups, ctas):
     env = dict(os.environ, DP_BUCKET=str(bucket), DP_DTYPE=dtype, DP_MODE=mode, DP_GROUPS=str(groups),
                DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp),
                DP_UPDATE_CTAS=str(upd), DP_INGEST=str(ingest),
-               DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width), DP_HOST=str(host))
+               DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width), DP_HOST=str(host),
+               DP_CLIP=str(clip))
     visible = os.environ.get("CUDA_VISIBLE_DEVICES")
     ids = visible.split(",") if visible else [str(i) for i in range(torch.cuda.device_count())]
     env["CUDA_VISIBLE_DEVICES"] = ",".join(ids[:world])
