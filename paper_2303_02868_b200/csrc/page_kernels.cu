@@ -189,11 +189,12 @@ accumulate_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restric
         for (int j = 0; j < 16; ++j) {
           uint32_t& w = ra[k][j >> 1];
           const uint16_t bits = (j & 1) ? (uint16_t)(w >> 16) : (uint16_t)(w & 0xffffu);
-          const float r = Elem<DDT>::widen(Elem<DDT>::narrow(__fadd_rn(0.0f, widen_bits<SDT>(bits))));
+          const TD nv = Elem<DDT>::narrow(__fadd_rn(0.0f, widen_bits<SDT>(bits)));   // stored as is
+          const float r = Elem<DDT>::widen(nv);
           bad |= !is_finite(r);
-          sq += __fmul_rn(r, r);
+          sq = __fmaf_rn(r, r, sq);   // the norm only feeds clipping: one rounding per term is fine
           if constexpr (LEDGER) ls.add(r);
-          const uint32_t ob = narrow_bits<DDT>(r);
+          const uint32_t ob = (uint32_t)(*reinterpret_cast<const uint16_t*>(&nv));
           w = (j & 1) ? ((w & 0xffffu) | (ob << 16)) : ((w & 0xffff0000u) | ob);
         }
         st_u8(static_cast<TD*>(dst) + c.dst_off + e, ra[k]);
