@@ -252,7 +252,7 @@ def run_reference(args):
 
 # ---- the GPU arm ----------------------------------------------------------------------
 
-def build_state(args, device, world=1, rank=0, pool_alloc=None):
+def build_state(args, device, world=1, rank=0, pool_alloc=None, double_buffered=False):
     import torch
     from paper_2303_02868_b200 import lockfree as LF
     from paper_2303_02868_b200 import workloads as W
@@ -269,7 +269,8 @@ def build_state(args, device, world=1, rank=0, pool_alloc=None):
               for n in numels]
     buf = LF.ParamBuffer(params, dtype=args.dtype, page_bytes=page, device=device, layout=layout,
                          pool_alloc=pool_alloc)
-    ms = LF.MasterState(params, page_bytes=page, device=device, layout=layout)
+    ms = LF.MasterState(params, page_bytes=page, device=device, layout=layout,
+                        double_buffered=double_buffered)
     del params
     torch.cuda.empty_cache()
     return specs, page, layout, buf, ms
@@ -537,6 +538,9 @@ def main():
     ap.add_argument("--dp-reduce-ctas", type=int, default=0,
                     help="pipelined DP step: persistent grid of the reduce kernel (0 = one CTA per "
                          "chunk) so it shares the SMs with the previous group's update")
+    ap.add_argument("--dp-onepass", type=int, default=0, choices=[0, 1],
+                    help="fused P2P DP step as ONE kernel over a double-buffered fp32 state "
+                         "(reduce-scatter + update + all-gather, commit after a flag merge)")
     ap.add_argument("--dp-mode", default="p2p", choices=["nccl", "p2p", "nvls"],
                     help="N>1 collectives: NCCL RS/AG, or fused kernels over NVLink peer memory "
                          "(p2p) / NVSwitch multicast (nvls)")

@@ -255,6 +255,35 @@ int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_grou
                     float* p32, float* m32, float* v32,
                     const uint64_t* peer_p16, int n_peers, void* mc_p16, int p16_dtype,
                     const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream);
+/* The DP page step as ONE pass (round 2; state double-buffered per layer):
+ * per owned chunk, pull the chunk's 16-bit gradient from every rank's pool
+ * (peer_g16: every rank's gradient pool base in rank order, the caller's
+ * own included; offsets = chunk g_off + group g_shift), sum in f32 in rank
+ * order and round once (the bits of hm_dp_reduce_check), run the page-Adam
+ * chain (hiermem/lockfree.py:135-141) on the layer's current state buffer
+ * (state_sel[group] selects buffer 0 or 1 of each [2 x state_elems] pool)
+ * and write the OTHER buffer, publish the new 16-bit page into every rank's
+ * pool (peer_p16), and OR the layer's non-finite flag into nonfinite[flag].
+ * Speculative: the prologue must have run on a copy of steps[], and
+ * hm_dp_onepass_finalize commits after a cross-rank barrier. */
+int hm_dp_onepass_update(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* groups,
+                         const hm_group_rt* rt, const uint32_t* state_sel, int64_t state_elems,
+                         const uint64_t* peer_g16, const uint64_t* peer_p16, int n_peers, int dtype,
+                         float* p32, float* m32, float* v32, uint32_t* nonfinite,
+                         const hm_adam_hyper* hyper, void* stream);
+/* Commit of a one-pass step: per layer, flag = OR over the ranks' flags
+ * (peer_flags); applied: steps[l] = steps_spec[l] and state_sel[l] flips;
+ * rejected: both stay (hiermem/lockfree.py:133-134, 163-164).  applied[]
+ * and the ledger row's applied column (ledger_out[2l+1]) are nullable. */
+int hm_dp_onepass_finalize(const uint64_t* peer_flags, int n_peers, int n_layers, int32_t* steps,
+                           const int32_t* steps_spec, uint32_t* state_sel, uint32_t* applied,
+                           double* ledger_out, void* stream);
+/* Publish the unchanged parameters of the owned pages of every REJECTED
+ * layer again (the one-pass update published speculatively). */
+int hm_dp_republish_rejected(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* groups,
+                             const uint32_t* applied, const uint32_t* state_sel, int64_t state_elems,
+                             const float* p32, const uint64_t* peer_p16, int n_peers, int dtype,
+                             void* stream);
 /* Process-wide DEFAULTS of hm_launch_opts.ag_publish / grid_ctas for
  * hm_adam_main_ag.  Publish epilogue over P2P: 0 = every thread stores its
  * 16 B granules into every peer (default); 1 (or 2) = the CTA stages its

@@ -20,7 +20,7 @@ LIB = PKG / "libhm_page.so"
 OBJ = PKG / "_obj"
 
 SOURCES = ["hm_error.cpp", "pagetable.cpp", "page_adam.cu", "page_adam_tma.cu", "page_kernels.cu",
-           "page_dp.cu"]
+           "page_dp.cu", "page_dp_onepass.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: the reference chain is one numpy ufunc per operator, so no

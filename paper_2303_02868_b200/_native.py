@@ -102,6 +102,10 @@ SIGNATURES = {
     "hm_dp_flags_merge": (_INT, [_P, _P, _INT, _INT, _P, _P, _P]),
     "hm_adam_main_ag": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT, _P, _INT,
                                C.POINTER(AdamHyperC), _OPTS, _P]),
+    "hm_dp_onepass_update": (_INT, [_P, _I64, _P, _P, _P, _I64, _P, _P, _INT, _INT, _P, _P, _P, _P,
+                                     C.POINTER(AdamHyperC), _P]),
+    "hm_dp_onepass_finalize": (_INT, [_P, _INT, _INT, _P, _P, _P, _P, _P, _P]),
+    "hm_dp_republish_rejected": (_INT, [_P, _I64, _P, _P, _P, _I64, _P, _P, _INT, _INT, _P]),
     "hm_accumulate": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P, _P, _OPTS, _P]),
     "hm_stats_take": (_INT, [_P, _I32, _P, _P, _P, _P, _P]),
     "hm_cast": (_INT, [_P, _INT, _P, _INT, _P, _I64, _P]),

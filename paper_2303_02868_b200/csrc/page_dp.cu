@@ -264,7 +264,9 @@ __global__ void flags_merge_kernel(PeerPtrs flag_peers, PeerPtrs sumsq_peers, in
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
     uint32_t f = 0;
     double s = 0.0;
-    for (int r = 0; r < flag_peers.n; ++r) {
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {   // constant indices: no local-memory copy of the peer table
+      if (r >= flag_peers.n) break;
       f |= reinterpret_cast<const volatile uint32_t*>(flag_peers.p[r])[l];
       if (sumsq_out) s += reinterpret_cast<const volatile double*>(sumsq_peers.p[r])[l];
     }

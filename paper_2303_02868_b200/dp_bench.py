@@ -75,7 +75,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     if fused:
         try:   # symmetric (peer-mapped) pools; every rank must agree on the outcome
             specs, page, layout, buf, ms = build_state(args, device, world, rank,
-                                                       pool_alloc=symmetric_alloc)
+                                                       pool_alloc=symmetric_alloc,
+                                                       double_buffered=bool(args.dp_onepass))
             dp = FusedShardedPageStep(buf, ms, mode=args.dp_mode)
             ok = torch.ones(1, device=device)
         except Exception as e:  # e.g. no peer mapping / multicast on this system
@@ -101,6 +102,9 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         # the transfer (C2/C4/C5, >= 1 GB of 16-bit pages), not for C1 (0.25 GB)
         big = 2 * P >= 1e9
         args.dp_groups, args.dp_reduce_ctas = (8, 128) if world == 2 and big else (1, 0)
+    if fused and dp.one_pass:
+        args.dp_groups = 1      # the one-pass kernel overlaps the exchange with the update itself
+        knobs = {}
     pipelined = fused and args.dp_groups > 1
 
     def do_step(**kw):   # launch settings travel with each launch (hm_launch_opts)
@@ -176,7 +180,12 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
 
     S = 2 * P                                  # the algorithmic 16-bit payload
     busbw = lambda ms_: S / (ms_ / 1e3) * (world - 1) / world / 1e9
-    if fused:
+    if fused and dp.one_pass:
+        phases = {"onepass_ms": parts["update_ag_ms"], "rs_and_ag_busbw_gbs": 2 * busbw(parts["update_ag_ms"]),
+                  "note": "one unpipelined instrumented step: the reduce-scatter, the update and the "
+                          "all-gather are ONE kernel (plus the flag merge / commit); the busbw counts both "
+                          "exchanges over its time"}
+    elif fused:
         phases = {"rs_ms": parts["rs_ms"], "rs_busbw_gbs": busbw(parts["rs_ms"]),
                   "update_ag_ms": parts["update_ag_ms"],
                   "ag_busbw_gbs": busbw(parts["update_ag_ms"]),
@@ -190,7 +199,7 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                   "note": "NCCL collectives timed alone"}
     link = measure_nvlink(device, world, rank)
     pipe = None
-    if fused:
+    if fused and not dp.one_pass:
         pipe = lambda ready, res: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
                                                     ready=ready, results_to=res, **knobs)
     e2e = run_e2e(args, buf, ms, do_step, flat, layout, pipe) if args.e2e_steps > 0 else None
@@ -217,7 +226,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         "run": {"bucket_pages_per_rank": layout.K, "buckets": layout.num_buckets,
                 "sharding": "page-sharded ZeRO-3 (owner = page % N)",
                 "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
-                "dp_mode": args.dp_mode if fallback is None else f"nccl (fallback: {fallback})",
+                "dp_mode": (args.dp_mode + (" one-pass" if fused and dp.one_pass else "")) if fallback is None
+                           else f"nccl (fallback: {fallback})",
                 "dp_groups": args.dp_groups if pipelined else 1,
                 "dp_reduce_ctas": args.dp_reduce_ctas if pipelined else 0,
                 "dp_update_ctas": args.dp_update_ctas if pipelined else 0,

@@ -468,21 +468,46 @@ class MasterState(_Paged):
     physical placement is HBM here (the pinned-host tier is swap.py)."""
 
     def __init__(self, params, tier: str = "SSD", *, page_bytes: int = PAGE_BYTES_DEFAULT,
-                 device=None, layout: PageLayout | None = None, world_size: int = 1, rank: int = 0):
+                 device=None, layout: PageLayout | None = None, world_size: int = 1, rank: int = 0,
+                 double_buffered: bool = False):
+        """``double_buffered``: two copies of every state pool, the current
+        one per layer selected on the device (``_state_sel``) — what the
+        one-pass DP step (sharding.FusedShardedPageStep) updates
+        speculatively: it writes the other copy and flips the layer only if
+        the layer was applied.  Such a state is updated by that step only."""
         self._init_paged(params, page_bytes, device, layout, world_size, rank)
         self.tier = tier
         lay = self.layout
+        self._db = bool(double_buffered)
         st = self._stream()
         with D.on(st):
-            self.p32_pool = torch.zeros(lay.elems_state, dtype=torch.float32, device=self.device)
+            n = lay.elems_state * (2 if self._db else 1)
+            self.p32_pool = torch.zeros(n, dtype=torch.float32, device=self.device)
             self.m32_pool = torch.zeros_like(self.p32_pool)
             self.v32_pool = torch.zeros_like(self.p32_pool)
             self._steps = torch.zeros(self.num_layers, dtype=torch.int32, device=self.device)
             self._applied = torch.zeros(self.num_layers, dtype=torch.int32, device=self.device)
+            if self._db:
+                self._state_sel = torch.zeros(self.num_layers, dtype=torch.int32, device=self.device)
+                self._steps_spec = torch.zeros_like(self._steps)
         self._step_bound = [0] * self.num_layers
         self._prepub = [None] * self.num_layers   # (buffer ref, token) of a pre-published p16
         for l, p in enumerate(params):
             self._pack_p32(l, p, st)
+
+    def _current(self, pool, layer):
+        """The layer's current copy of a state pool (double-buffered: the
+        device's selection, read back)."""
+        if not self._db:
+            return pool
+        es = self.layout.elems_state
+        sel = int(self._state_sel[layer].item())
+        return pool[sel * es:(sel + 1) * es]
+
+    def _single_buffered(self, what: str):
+        if self._db:
+            raise ConfigError(f"{what}: a double-buffered MasterState is updated by the one-pass "
+                              "DP step only")
 
     # reference attributes ------------------------------------------------------
     @property
@@ -491,18 +516,18 @@ class MasterState(_Paged):
 
     @property
     def m32(self):
-        return _LayerView(self, lambda l: self._unpack(self.m32_pool, l))
+        return _LayerView(self, lambda l: self._unpack(self._current(self.m32_pool, l), l))
 
     @property
     def v32(self):
-        return _LayerView(self, lambda l: self._unpack(self.v32_pool, l))
+        return _LayerView(self, lambda l: self._unpack(self._current(self.v32_pool, l), l))
 
     @property
     def steps(self) -> list[int]:
         return [int(x) for x in self._steps.cpu().tolist()]
 
     def _p32_of(self, layer):
-        out = self._unpack(self.p32_pool, layer)
+        out = self._unpack(self._current(self.p32_pool, layer), layer)
         if isinstance(out, torch.Tensor) and self._prepub[layer] is not None:
             # the fast update_layer already cast these values into the
             # buffer's inactive publish pages: publish() of this unmodified
@@ -518,7 +543,7 @@ class MasterState(_Paged):
             src = D.to_device_flat(value, self.device)
             if src.dtype != torch.float32:
                 src = src.float()
-        self._cast(src, N.DT_F32, self.p32_pool, N.DT_F32,
+        self._cast(src, N.DT_F32, self._current(self.p32_pool, layer), N.DT_F32,
                    self.layout.seg_chunks(layer, "state", owned_only=True), st)
 
     def _unpack(self, pool, layer, stream=None):
@@ -553,6 +578,7 @@ class MasterState(_Paged):
         isfinite pass), and casts the new masters into the buffer's inactive
         publish pages, so the ``publish`` that follows is a record flip."""
         self._check_layer(layer)
+        self._single_buffered("update_layer")
         st = self._stream(stream)
         self._prepub[layer] = None
         h = getattr(grad, "_hm_taken", None) if isinstance(grad, torch.Tensor) else None
@@ -1040,6 +1066,7 @@ def sweep(buffer: ParamBuffer, masters: MasterState, hyper: AdamHyper, layers=No
     if masters.layout.numels != lay.numels or masters.layout.page_bytes != lay.page_bytes \
             or masters.layout.world_size != lay.world_size:
         raise ConfigError("buffer and masters were built on different page tables")
+    masters._single_buffered("sweep")
     st = buffer._stream(stream)
     order = list(reversed(range(buffer.num_layers))) if layers is None else list(layers)
     sel = [l for l in order if buffer._pending[l] > 0]

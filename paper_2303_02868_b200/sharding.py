@@ -127,6 +127,8 @@ class ShardedPageStep:
     the same world-sharded PageLayout (MasterState holds owned pages only)."""
 
     def __init__(self, buffer, masters, group=None, comm_stream=None):
+        if getattr(masters, "_db", False):
+            raise ConfigError("a double-buffered state is updated by FusedShardedPageStep's one-pass step")
         lay = buffer.layout
         if masters.layout is not lay and (masters.layout.numels != lay.numels
                                           or masters.layout.world_size != lay.world_size):
@@ -267,6 +269,11 @@ class FusedShardedPageStep:
         self._adam_chunks = lay.adam_chunks(range(L), "pool", owned_only=True)
         # pinned-host / SSD state tier: the state is streamed in step()
         self.host_tier = hasattr(masters, "stream_update")
+        # double-buffered state: step() is ONE speculative pass (reduce-scatter
+        # + update + all-gather in one kernel, commit after a flag merge)
+        self.one_pass = bool(getattr(masters, "_db", False))
+        if self.one_pass and mode != "p2p":
+            raise ConfigError("the one-pass DP step pulls the gradient with P2P loads (mode='p2p')")
 
     @staticmethod
     def _arr(ptrs):
@@ -343,6 +350,9 @@ class FusedShardedPageStep:
         if self.host_tier:
             raise ConfigError("the layer-group pipeline keeps the state in HBM; a host/SSD-tier "
                               "DP step streams the state in step()")
+        if self.one_pass:
+            raise ConfigError("a double-buffered state is updated by the one-pass step(): "
+                              "its reduce already overlaps the update inside one kernel")
         st = buf._stream(stream)
         L = buf.num_layers
         if any(p == 0 for p in buf._pending):
@@ -494,6 +504,11 @@ class FusedShardedPageStep:
 
         lib, eng = N.lib(), ms._eng
         clip = getattr(hyper, "max_norm", 0.0) > 0
+        if self.one_pass:
+            if clip:
+                raise ConfigError("global grad-norm clipping needs the norm before the update: "
+                                  "the one-pass step cannot clip (use a single-buffered state)")
+            return self._step_one_pass(hyper, st, mark, marks, timings)
         with torch.cuda.stream(st):
             mark("start")
             self.flags_local.zero_()
@@ -535,6 +550,64 @@ class FusedShardedPageStep:
         else:
             launch(self._adam_chunks, (D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool)))
         with torch.cuda.stream(st):
+            mark("adam")
+            self.h_p.barrier(channel=0)                          # published pages landed everywhere
+            mark("ag")
+            done = torch.cuda.Event()
+            done.record(st)
+            self._last_done = done
+        t.finish(consumed_flags=False)
+        if timings is not None:
+            timings["_marks"] = marks
+        return list(range(L))
+
+    def _step_one_pass(self, hyper, st, mark, marks, timings):
+        """barrier -> speculative prologue (on a copy of the step counters) ->
+        hm_dp_onepass_update (pull every rank's gradient of the owned pages,
+        reduce, update into the other state copy, publish to every rank) ->
+        barrier -> hm_dp_onepass_finalize (merge the flags, commit steps and
+        state copies of applied layers) -> republish rejected layers ->
+        barrier.  One data-path kernel; the reduced gradient is never written."""
+        buf, ms, lay = self.buffer, self.masters, self.layout
+        L = buf.num_layers
+        gsel = buf._gsel[0]
+        lib, eng = N.lib(), ms._eng
+        with torch.cuda.stream(st):
+            mark("start")
+            self.flags_local.zero_()
+            ms._steps_spec.copy_(ms._steps)
+            self.h_g.barrier(channel=0)                          # every rank's gradients are complete
+            mark("rs_start")
+            mark("rs")
+            mark("check")
+        t = UpdateTicket(buf, range(L), flag_of=lambda l: l)
+        for l in range(L):
+            ms._prepub[l] = None
+        dgroups = eng.desc.table(t.groups, st)
+        rt = eng.rt_scratch(L, st)
+        bc, bc_len = ms._bias(hyper, range(L))
+        hc = D.hyper_c(hyper)
+        # speculative: every layer assumed finite, steps advanced in the copy;
+        # the take record of the ledger is written here, its applied column
+        # by the finalize
+        D.check(lib.hm_adam_prologue(D.ptr(dgroups), L, D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
+                                     D.ptr(ms._steps_spec), None, None, None, 1,
+                                     t.lsum(gsel * L) or None, t.ledger_out or None, D.sptr(st)))
+        ac = self._adam_chunks
+        gp, pp = self._arr(self.g_ptrs), self._arr(self.p_ptrs)
+        es = lay.elems_state
+        D.check(lib.hm_dp_onepass_update(D.ptr(eng.desc.static(ac)), len(ac), D.ptr(dgroups), D.ptr(rt),
+                                         D.ptr(ms._state_sel), es, gp, pp, self.n, buf._dt,
+                                         D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool),
+                                         D.ptr(self.flags_local), hc, D.sptr(st)))
+        with torch.cuda.stream(st):
+            self.h_f.barrier(channel=0)                          # every rank's flags are final
+            D.check(lib.hm_dp_onepass_finalize(self._arr(self.f_ptrs), self.n, L, D.ptr(ms._steps),
+                                               D.ptr(ms._steps_spec), D.ptr(ms._state_sel),
+                                               D.ptr(ms._applied), t.ledger_out or None, D.sptr(st)))
+            D.check(lib.hm_dp_republish_rejected(D.ptr(eng.desc.static(ac)), len(ac), D.ptr(dgroups),
+                                                 D.ptr(ms._applied), D.ptr(ms._state_sel), es,
+                                                 D.ptr(ms.p32_pool), pp, self.n, buf._dt, D.sptr(st)))
             mark("adam")
             self.h_p.barrier(channel=0)                          # published pages landed everywhere
             mark("ag")

@@ -51,8 +51,10 @@ def main():
         path = os.path.join(tempfile.gettempdir(), f"hm_dp_state_{os.getpid()}_{rank}.bin")
         ms = SSDMasterState([torch.from_numpy(p) for p in params], path, page_bytes=PAGE, device=dev,
                             layout=lay, group_pages=2, world_size=world, rank=rank)
-    else:
-        ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay)
+    else:   # DP_ONEPASS=1: double-buffered state, the one-pass fused step
+        ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay,
+                            double_buffered=os.environ.get("DP_ONEPASS", "0") == "1")
+    onepass = getattr(ms, "_db", False)
     step = ShardedPageStep(buf, ms) if mode == "nccl" else FusedShardedPageStep(buf, ms, mode=mode)
     from paper_2303_02868_b200 import _native as NL
     NL.check(NL.lib().hm_set_ag_publish(int(os.environ.get("DP_AG_PUBLISH", "0"))))
@@ -137,6 +139,8 @@ def main():
                 red = O.to16(acc, dtype)
             captured = red.copy()
             for s in lay.segments[l]:
+                if onepass:   # the one-pass step never writes the reduced gradient back
+                    continue
                 off = lay.slot16(s.page) * lay.E + s.off
                 got = gpool[off:off + s.n]
                 want = red[s.pos:s.pos + s.n]

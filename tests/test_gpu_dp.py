@@ -30,7 +30,8 @@ CASES = [
     (2, "bf16", "p2p", 1, "ld128"),   # the 16 B-load reduce (256-bit loads are the default)
     (2, "bf16", "p2p", 1, "host"), (3, "fp16", "p2p", 1, "host"),   # fp32 state on the pinned-host tier
     (2, "bf16", "p2p", 1, "ssd"),    # fp32 state in a file per rank (SSD tier)
-    (2, "bf16", "p2p", 1, "clip"), (2, "fp16", "nccl", 1, "clip")]   # global grad-norm clip over all ranks
+    (2, "bf16", "p2p", 1, "clip"), (2, "fp16", "nccl", 1, "clip"),   # global grad-norm clip over all ranks
+    (2, "bf16", "p2p", 1, "onepass"), (3, "fp16", "p2p", 1, "onepass")]   # ONE fused RS+update+AG kernel
 SMOKE2 = [CASES[1], CASES[3], CASES[6], CASES[12], CASES[17]]
 
 
@@ -56,9 +57,11 @@ def test_dp_step_two_ranks(bucket, dtype, mode, groups, ctas):
 
 def _run(world, bucket, dtype, mode, groups, ctas):
     agp, upd, ingest, green, width, ld256, host = 0, 0, 0, 0, 0, 0, 0
-    clip = 0.0
+    clip, onepass = 0.0, 0
     if ctas == "clip":
         clip, ctas = 1.0, 0
+    elif ctas == "onepass":
+        onepass, ctas = 1, 0
     elif ctas in ("host", "ssd"):
         host, ctas = (1 if ctas == "host" else "ssd"), 0
     elif ctas == "ld128":
@@ -77,7 +80,7 @@ def _run(world, bucket, dtype, mode, groups, ctas):
                DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp),
                DP_UPDATE_CTAS=str(upd), DP_INGEST=str(ingest),
                DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width), DP_HOST=str(host),
-               DP_CLIP=str(clip))
+               DP_CLIP=str(clip), DP_ONEPASS=str(onepass))
     visible = os.environ.get("CUDA_VISIBLE_DEVICES")
     ids = visible.split(",") if visible else [str(i) for i in range(torch.cuda.device_count())]
     env["CUDA_VISIBLE_DEVICES"] = ",".join(ids[:world])

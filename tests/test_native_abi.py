@@ -45,7 +45,7 @@ def test_kernels_do_not_spill():
     """Every data-path kernel in the library keeps its working set in
     registers: no local memory / stack (a spill or a runtime-indexed peer
     table turns into extra HBM traffic — it once cost the update+AG kernel
-    2 GB per step).  The tiny per-layer flag merge is exempt."""
+    2 GB per step)."""
     import shutil
     import subprocess
     import pytest
@@ -56,8 +56,7 @@ def test_kernels_do_not_spill():
     out = subprocess.run([tool, "-res-usage", str(lib)], capture_output=True, text=True, check=True).stdout
     funcs = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+) SHARED:\d+ LOCAL:(\d+)", out)
     assert len(funcs) > 20
-    bad = [(f, stack, local) for f, _, stack, local in funcs
-           if (int(stack) or int(local)) and "flags_merge" not in f]
+    bad = [(f, stack, local) for f, _, stack, local in funcs if int(stack) or int(local)]
     assert not bad, bad
 
 

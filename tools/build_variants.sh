@@ -8,7 +8,7 @@ PKG=paper_2303_02868_b200
 while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   obj=$PKG/_obj_$name; mkdir -p $obj
-  for src in hm_error.cpp pagetable.cpp page_adam.cu page_adam_tma.cu page_kernels.cu page_dp.cu; do
+  for src in hm_error.cpp pagetable.cpp page_adam.cu page_adam_tma.cu page_kernels.cu page_dp.cu page_dp_onepass.cu; do
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -fmad=false -Xcompiler -fPIC \
       -Xcompiler -O3 --expt-relaxed-constexpr $flags -I include -c $PKG/csrc/$src -o $obj/${src%.*}.o &
   done
