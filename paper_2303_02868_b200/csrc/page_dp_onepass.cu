@@ -32,8 +32,12 @@
 namespace hm {
 namespace {
 
+// 512 threads x one granule per thread, two resident CTAs (64 registers) up
+// to 4 peers: the remote loads need warps in flight more than granules per
+// thread (N=2, C2: 4.04 ms vs 4.70 with 256 threads x 2).  Eight peers'
+// gradient granules do not fit 64 registers: one CTA of 94.
 template <int DT, int NP, int NT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, NP <= 4 ? 2 : 1)
 onepass_kernel(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ groups,
                const hm_group_rt* __restrict__ rt, const uint32_t* __restrict__ state_sel, uint64_t es,
                PeerPtrs gpeers, PeerPtrs ppeers, float* __restrict__ p32, float* __restrict__ m32,
@@ -158,13 +162,10 @@ republish_kernel(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch
 using OnepassFn = void (*)(const hm_adam_chunk*, const hm_group_launch*, const hm_group_rt*, const uint32_t*,
                            uint64_t, PeerPtrs, PeerPtrs, float*, float*, float*, uint32_t*, hm_adam_hyper);
 
-// 256 threads x 2 granules while the peer loads fit the registers (N <= 2),
-// 512 x 1 beyond.
 template <int DT>
 OnepassFn pick_onepass_dt(int n, int* threads) {
-  if (n <= 2) { *threads = 256; return onepass_kernel<DT, 2, 256>; }
   *threads = 512;
-  return n <= 4 ? onepass_kernel<DT, 4, 512> : onepass_kernel<DT, 8, 512>;
+  return n <= 2 ? onepass_kernel<DT, 2, 512> : n <= 4 ? onepass_kernel<DT, 4, 512> : onepass_kernel<DT, 8, 512>;
 }
 
 }  // namespace
