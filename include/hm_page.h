@@ -265,12 +265,13 @@ int hm_adam_main_ag(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_grou
  * and write the OTHER buffer, publish the new 16-bit page into every rank's
  * pool (peer_p16), and OR the layer's non-finite flag into nonfinite[flag].
  * Speculative: the prologue must have run on a copy of steps[], and
- * hm_dp_onepass_finalize commits after a cross-rank barrier. */
+ * hm_dp_onepass_finalize commits after a cross-rank barrier.
+ * opts.reduce_width: minimum peer-array width of the kernel (nullable). */
 int hm_dp_onepass_update(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* groups,
                          const hm_group_rt* rt, const uint32_t* state_sel, int64_t state_elems,
                          const uint64_t* peer_g16, const uint64_t* peer_p16, int n_peers, int dtype,
                          float* p32, float* m32, float* v32, uint32_t* nonfinite,
-                         const hm_adam_hyper* hyper, void* stream);
+                         const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream);
 /* Commit of a one-pass step: per layer, flag = OR over the ranks' flags
  * (peer_flags); applied: steps[l] = steps_spec[l] and state_sel[l] flips;
  * rejected: both stay (hiermem/lockfree.py:133-134, 163-164).  applied[]

@@ -103,7 +103,7 @@ SIGNATURES = {
     "hm_adam_main_ag": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT, _P, _INT,
                                C.POINTER(AdamHyperC), _OPTS, _P]),
     "hm_dp_onepass_update": (_INT, [_P, _I64, _P, _P, _P, _I64, _P, _P, _INT, _INT, _P, _P, _P, _P,
-                                     C.POINTER(AdamHyperC), _P]),
+                                     C.POINTER(AdamHyperC), _OPTS, _P]),
     "hm_dp_onepass_finalize": (_INT, [_P, _INT, _INT, _P, _P, _P, _P, _P, _P]),
     "hm_dp_republish_rejected": (_INT, [_P, _I64, _P, _P, _P, _I64, _P, _P, _INT, _INT, _P]),
     "hm_accumulate": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P, _P, _OPTS, _P]),

@@ -177,7 +177,7 @@ int hm_dp_onepass_update(const hm_adam_chunk* chunks, int64_t n_chunks, const hm
                          const hm_group_rt* rt, const uint32_t* state_sel, int64_t state_elems,
                          const uint64_t* peer_g16, const uint64_t* peer_p16, int n_peers, int dtype,
                          float* p32, float* m32, float* v32, uint32_t* nonfinite,
-                         const hm_adam_hyper* hyper, void* stream) {
+                         const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream) {
   if (!hyper || !rt) return hm_set_error(HM_ERR_INVALID, "hm_dp_onepass_update: missing hyper/rt");
   hm::PeerPtrs gp, pp;
   if (int rc = hm::make_peers(peer_g16, n_peers, &gp)) return rc;
@@ -185,8 +185,12 @@ int hm_dp_onepass_update(const hm_adam_chunk* chunks, int64_t n_chunks, const hm
   if (n_chunks < 0 || n_chunks > 0x7fffffffLL || state_elems < 0)
     return hm_set_error(HM_ERR_INVALID, "hm_dp_onepass_update: bad chunk count / state size");
   int threads = 256;
-  hm::OnepassFn fn = dtype == HM_DT_BF16 ? hm::pick_onepass_dt<HM_DT_BF16>(n_peers, &threads)
-                   : dtype == HM_DT_F16 ? hm::pick_onepass_dt<HM_DT_F16>(n_peers, &threads) : nullptr;
+  // opts.reduce_width: minimum peer-array width (8 runs the N=8 instantiation on a smaller box)
+  const int width = opts && opts->reduce_width > n_peers ? opts->reduce_width : n_peers;
+  if (width > hm::kMaxPeers)
+    return hm_set_error(HM_ERR_INVALID, "hm_dp_onepass_update: width %d > %d", width, hm::kMaxPeers);
+  hm::OnepassFn fn = dtype == HM_DT_BF16 ? hm::pick_onepass_dt<HM_DT_BF16>(width, &threads)
+                   : dtype == HM_DT_F16 ? hm::pick_onepass_dt<HM_DT_F16>(width, &threads) : nullptr;
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_dp_onepass_update: unsupported dtype %d", dtype);
   if (n_chunks == 0) return HM_OK;
   HM_REQUIRE_PTRS("hm_dp_onepass_update", chunks, groups, state_sel, p32, m32, v32, nonfinite);

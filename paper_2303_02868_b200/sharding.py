@@ -508,7 +508,7 @@ class FusedShardedPageStep:
             if clip:
                 raise ConfigError("global grad-norm clipping needs the norm before the update: "
                                   "the one-pass step cannot clip (use a single-buffered state)")
-            return self._step_one_pass(hyper, st, mark, marks, timings)
+            return self._step_one_pass(hyper, st, mark, marks, timings, reduce_width)
         with torch.cuda.stream(st):
             mark("start")
             self.flags_local.zero_()
@@ -561,7 +561,7 @@ class FusedShardedPageStep:
             timings["_marks"] = marks
         return list(range(L))
 
-    def _step_one_pass(self, hyper, st, mark, marks, timings):
+    def _step_one_pass(self, hyper, st, mark, marks, timings, reduce_width=-1):
         """barrier -> speculative prologue (on a copy of the step counters) ->
         hm_dp_onepass_update (pull every rank's gradient of the owned pages,
         reduce, update into the other state copy, publish to every rank) ->
@@ -599,7 +599,8 @@ class FusedShardedPageStep:
         D.check(lib.hm_dp_onepass_update(D.ptr(eng.desc.static(ac)), len(ac), D.ptr(dgroups), D.ptr(rt),
                                          D.ptr(ms._state_sel), es, gp, pp, self.n, buf._dt,
                                          D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool),
-                                         D.ptr(self.flags_local), hc, D.sptr(st)))
+                                         D.ptr(self.flags_local), hc, D.opts(reduce_width=reduce_width),
+                                         D.sptr(st)))
         with torch.cuda.stream(st):
             self.h_f.barrier(channel=0)                          # every rank's flags are final
             D.check(lib.hm_dp_onepass_finalize(self._arr(self.f_ptrs), self.n, L, D.ptr(ms._steps),

@@ -106,6 +106,8 @@ def main():
             step.step_pipelined(hyper, groups, reduce_ctas=int(os.environ.get("DP_REDUCE_CTAS", "0")),
                                 update_ctas=int(os.environ.get("DP_UPDATE_CTAS", "0")),
                                 reduce_sms=int(os.environ.get("DP_REDUCE_SMS", "0")))
+        elif onepass:
+            step.step(hyper, reduce_width=int(os.environ.get("DP_REDUCE_WIDTH", "0")) or -1)
         else:
             step.step(hyper)
         if ingest:
