@@ -538,9 +538,10 @@ def main():
     ap.add_argument("--dp-reduce-ctas", type=int, default=0,
                     help="pipelined DP step: persistent grid of the reduce kernel (0 = one CTA per "
                          "chunk) so it shares the SMs with the previous group's update")
-    ap.add_argument("--dp-onepass", type=int, default=0, choices=[0, 1],
+    ap.add_argument("--dp-onepass", type=int, default=-1, choices=[-1, 0, 1],
                     help="fused P2P DP step as ONE kernel over a double-buffered fp32 state "
-                         "(reduce-scatter + update + all-gather, commit after a flag merge)")
+                         "(reduce-scatter + update + all-gather, commit after a flag merge); "
+                         "-1 = auto (on at N=2, where it wins; profiles/r2_bench.md)")
     ap.add_argument("--dp-mode", default="p2p", choices=["nccl", "p2p", "nvls"],
                     help="N>1 collectives: NCCL RS/AG, or fused kernels over NVLink peer memory "
                          "(p2p) / NVSwitch multicast (nvls)")

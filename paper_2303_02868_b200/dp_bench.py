@@ -74,6 +74,11 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
     fallback = None
     if fused:
         try:   # symmetric (peer-mapped) pools; every rank must agree on the outcome
+            if args.dp_onepass < 0:   # auto: measured policy (profiles/r2_bench.md)
+                # N=2: one kernel beats the layer-group pipeline (4.04 vs 4.87 ms, C2);
+                # N>=4 the step is link-bound and the two-phase kernels move the
+                # bytes more efficiently (5.80 vs 5.98 ms)
+                args.dp_onepass = 1 if world == 2 and args.dp_mode == "p2p" else 0
             specs, page, layout, buf, ms = build_state(args, device, world, rank,
                                                        pool_alloc=symmetric_alloc,
                                                        double_buffered=bool(args.dp_onepass))
@@ -199,10 +204,13 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                   "note": "NCCL collectives timed alone"}
     link = measure_nvlink(device, world, rank)
     pipe = None
-    if fused and not dp.one_pass:
+    if fused and dp.one_pass:   # the one-pass kernel group by group as the gradient lands
+        pipe = lambda ready, res: dp.step(hyper, ready=ready)
+    elif fused:
         pipe = lambda ready, res: dp.step_pipelined(hyper, args.e2e_groups, reduce_ctas=args.dp_reduce_ctas,
                                                     ready=ready, results_to=res, **knobs)
-    e2e = run_e2e(args, buf, ms, do_step, flat, layout, pipe) if args.e2e_steps > 0 else None
+    e2e = run_e2e(args, buf, ms, do_step, flat, layout, pipe,
+                  with_results=not (fused and dp.one_pass)) if args.e2e_steps > 0 else None
     # Link-level bytes per direction per GPU for the step: P2P (and NCCL)
     # move (N-1)/N*S in for the reduce-scatter and (N-1)/N*S in for the
     # all-gather (the same out); NVLS reads the reduced S/N from the switch
@@ -302,7 +310,7 @@ def measure_nvlink(device, world, rank, nbytes: int = 1 << 29, reps: int = 5) ->
                    "slowest rank"}
 
 
-def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
+def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None, with_results=True):
     """The DP step through the public API with host buffers, per rank: H2D of
     this rank's whole 16-bit gradient from pinned memory + K3 accumulate, the
     sharded page step, and a D2H read of the per-layer applied flags.  Time =
@@ -342,7 +350,7 @@ def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None):
 
     dt_serial = timed(serial)
     dt_pipe = timed(pipelined) if pipe is not None else None
-    dt_res = timed(lambda it: pipelined(it, True)) if pipe is not None else None
+    dt_res = timed(lambda it: pipelined(it, True)) if pipe is not None and with_results else None
     dt = min(dt_serial, dt_pipe) if dt_pipe else dt_serial
     piped = bool(dt_pipe and dt_pipe <= dt_serial)
     P = sum(layout.numels)

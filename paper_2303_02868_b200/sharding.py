@@ -478,15 +478,20 @@ class FusedShardedPageStep:
         return list(range(L))
 
     def step(self, hyper, *, stream=None, ag_publish: int = -1, reduce_wide: int = -1,
-             reduce_width: int = -1, timings: dict | None = None):
+             reduce_width: int = -1, ready=None, timings: dict | None = None):
         """barrier -> reduce-scatter + check -> barrier -> flag merge ->
         prologue -> update with the all-gather epilogue -> barrier.  With a
         host (or SSD) state tier the update streams the owned state pages
         through HBM staging (the tier's pipeline) between the reduce and the
         all-gather: each rank moves 24 B x its owned params over its own PCIe
-        link, the 16-bit pages travel over NVLink as usual."""
+        link, the 16-bit pages travel over NVLink as usual.  ``ready`` (one-pass
+        step only; one event per layer group from ``lockfree.ingest``): the
+        one-pass kernel runs group by group as each group's gradient lands on
+        every rank — the commit waits for all of them anyway."""
         buf, ms, lay = self.buffer, self.masters, self.layout
         st = buf._stream(stream)
+        if ready is not None and not self.one_pass:
+            raise ConfigError("step(ready=...) streams the one-pass step; use step_pipelined(ready=...)")
         L = buf.num_layers
         if any(p == 0 for p in buf._pending):
             raise ConfigError("a DP page step needs a gradient for every layer on every rank")
@@ -508,7 +513,7 @@ class FusedShardedPageStep:
             if clip:
                 raise ConfigError("global grad-norm clipping needs the norm before the update: "
                                   "the one-pass step cannot clip (use a single-buffered state)")
-            return self._step_one_pass(hyper, st, mark, marks, timings, reduce_width)
+            return self._step_one_pass(hyper, st, mark, marks, timings, reduce_width, ready)
         with torch.cuda.stream(st):
             mark("start")
             self.flags_local.zero_()
@@ -561,7 +566,7 @@ class FusedShardedPageStep:
             timings["_marks"] = marks
         return list(range(L))
 
-    def _step_one_pass(self, hyper, st, mark, marks, timings, reduce_width=-1):
+    def _step_one_pass(self, hyper, st, mark, marks, timings, reduce_width=-1, ready=None):
         """barrier -> speculative prologue (on a copy of the step counters) ->
         hm_dp_onepass_update (pull every rank's gradient of the owned pages,
         reduce, update into the other state copy, publish to every rank) ->
@@ -576,7 +581,8 @@ class FusedShardedPageStep:
             mark("start")
             self.flags_local.zero_()
             ms._steps_spec.copy_(ms._steps)
-            self.h_g.barrier(channel=0)                          # every rank's gradients are complete
+            if ready is None:
+                self.h_g.barrier(channel=0)                      # every rank's gradients are complete
             mark("rs_start")
             mark("rs")
             mark("check")
@@ -596,11 +602,26 @@ class FusedShardedPageStep:
         ac = self._adam_chunks
         gp, pp = self._arr(self.g_ptrs), self._arr(self.p_ptrs)
         es = lay.elems_state
-        D.check(lib.hm_dp_onepass_update(D.ptr(eng.desc.static(ac)), len(ac), D.ptr(dgroups), D.ptr(rt),
-                                         D.ptr(ms._state_sel), es, gp, pp, self.n, buf._dt,
-                                         D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool),
-                                         D.ptr(self.flags_local), hc, D.opts(reduce_width=reduce_width),
-                                         D.sptr(st)))
+        if ready is None:
+            parts = [(None, ac)]
+        else:   # one launch per layer group, each once its gradient landed on every rank
+            cache = self.__dict__.setdefault("_onepass_parts", {})
+            if len(ready) not in cache:
+                from .lockfree import layer_groups
+                slots = ac["slot"]
+                cache[len(ready)] = [ac[(slots >= grp[0]) & (slots <= grp[-1])].copy()
+                                     for grp in layer_groups(lay.numels, len(ready))]
+            parts = list(zip(ready, cache[len(ready)]))
+        for ev, chunks in parts:
+            if ev is not None:
+                st.wait_event(ev)
+                with torch.cuda.stream(st):
+                    self.h_g.barrier(channel=0)                  # this group landed on every rank
+            D.check(lib.hm_dp_onepass_update(D.ptr(eng.desc.static(chunks)), len(chunks), D.ptr(dgroups),
+                                             D.ptr(rt), D.ptr(ms._state_sel), es, gp, pp, self.n, buf._dt,
+                                             D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool),
+                                             D.ptr(self.flags_local), hc, D.opts(reduce_width=reduce_width),
+                                             D.sptr(st)))
         with torch.cuda.stream(st):
             self.h_f.barrier(channel=0)                          # every rank's flags are final
             D.check(lib.hm_dp_onepass_finalize(self._arr(self.f_ptrs), self.n, L, D.ptr(ms._steps),

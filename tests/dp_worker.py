@@ -99,7 +99,9 @@ def main():
         else:
             buf.accumulate_flat(t.to(dev), it)
         gsel = buf._gsel[0]
-        if ingest:   # ... and this rank's owned published pages come back to the host
+        if ingest and onepass:   # the one-pass kernel group by group as the gradient lands
+            step.step(hyper, ready=ready)
+        elif ingest:   # ... and this rank's owned published pages come back to the host
             out_host = torch.empty(sum(SIZES), dtype=buf._t16).pin_memory()
             step.step_pipelined(hyper, groups, ready=ready, results_to=out_host)
         elif groups > 1 and mode != "nccl":
@@ -110,7 +112,7 @@ def main():
             step.step(hyper, reduce_width=int(os.environ.get("DP_REDUCE_WIDTH", "0")) or -1)
         else:
             step.step(hyper)
-        if ingest:
+        if ingest and not onepass:
             torch.cuda.synchronize()
             pub = buf.p16_pool[buf._psel[0]].view(torch.int16).cpu()
             host16 = out_host.view(torch.int16)

@@ -32,7 +32,8 @@ CASES = [
     (2, "bf16", "p2p", 1, "ssd"),    # fp32 state in a file per rank (SSD tier)
     (2, "bf16", "p2p", 1, "clip"), (2, "fp16", "nccl", 1, "clip"),   # global grad-norm clip over all ranks
     (2, "bf16", "p2p", 1, "onepass"), (3, "fp16", "p2p", 1, "onepass"),   # ONE fused RS+update+AG kernel
-    (2, "bf16", "p2p", 1, "onepass8")]   # ... its 8-peer instantiation
+    (2, "bf16", "p2p", 1, "onepass8"),   # ... its 8-peer instantiation
+    (2, "bf16", "p2p", 4, "onepass_ingest")]   # ... group by group while the host gradient arrives
 SMOKE2 = [CASES[1], CASES[3], CASES[6], CASES[12], CASES[17]]
 
 
@@ -61,8 +62,9 @@ def _run(world, bucket, dtype, mode, groups, ctas):
     clip, onepass = 0.0, 0
     if ctas == "clip":
         clip, ctas = 1.0, 0
-    elif ctas in ("onepass", "onepass8"):
-        onepass, width, ctas = 1, (8 if ctas == "onepass8" else 0), 0
+    elif ctas in ("onepass", "onepass8", "onepass_ingest"):
+        onepass, width, ingest = 1, (8 if ctas == "onepass8" else 0), int(ctas == "onepass_ingest")
+        ctas = 0
     elif ctas in ("host", "ssd"):
         host, ctas = (1 if ctas == "host" else "ssd"), 0
     elif ctas == "ld128":
