@@ -364,9 +364,9 @@ def run_e2e(args, buf, ms, do_step, flat, layout, pipe=None, with_results=True):
                 "note": "step_pipelined(results_to=...): every rank also returns its owned published pages "
                         "(per rank, disjoint: the whole model once per step); the ranks share the host's "
                         "PCIe/memory bandwidth"},
-            "api": ("lockfree.ingest(pinned host gradient, %d layer groups) -> "
-                    "FusedShardedPageStep.step_pipelined(ready=...) -> applied flags to host, every rank"
-                    % args.e2e_groups) if piped else
+            "api": ("lockfree.ingest(pinned host gradient, %d layer groups) -> FusedShardedPageStep.%s"
+                    "(ready=...) -> applied flags to host, every rank"
+                    % (args.e2e_groups, "step" if not with_results else "step_pipelined")) if piped else
                    "ParamBuffer.accumulate_flat(pinned host gradient) + sharded page step + "
                    "applied flags to host, every rank"}
 
