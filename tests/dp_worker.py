@@ -208,9 +208,17 @@ def main():
                 d16 = np.abs(p16[off:off + s.n].astype(np.int32) - want16[s.pos:s.pos + s.n].astype(np.int32))
                 if d16.max(initial=0) > 1:
                     failures.append(f"layer{l} page{s.page}: all-gathered p16 off by {d16.max()} ulp")
+                # 1e-6 relative, or 1e-6 of the step size lr near zero, where the
+                # masters are a difference of nearly equal terms (after three
+                # updates of ~lr some elements sit at ~1e-7)
                 if lay.owned(s) and not np.allclose(mp[s.pos:s.pos + s.n], om.p32[l][s.pos:s.pos + s.n],
-                                                    rtol=1e-6, atol=1e-12):
-                    failures.append(f"layer{l} page{s.page}: owned p32 beyond 1e-6 relative")
+                                                    rtol=1e-6, atol=1e-6 * 1e-3):
+                    a, b = mp[s.pos:s.pos + s.n], om.p32[l][s.pos:s.pos + s.n]
+                    rel = np.abs(a - b) / np.maximum(np.abs(b), 1e-30)
+                    i = int(np.argmax(rel))
+                    failures.append(f"layer{l} page{s.page}: owned p32 beyond 1e-6 relative "
+                                    f"(max {rel[i]:.3g} at {i}: {a[i]!r} vs {b[i]!r}; "
+                                    f"{int((rel > 1e-6).sum())} of {s.n})")
                 continue
             if not np.array_equal(p16[off:off + s.n], want16[s.pos:s.pos + s.n]):
                 failures.append(f"layer{l} page{s.page}: all-gathered p16 differs")
