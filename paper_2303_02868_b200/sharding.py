@@ -13,7 +13,9 @@ Here they move real bytes over NVLink/NVSwitch, two ways:
   owned page from every peer and fuses the finite flag / norm
   (hm_dp_reduce_check), and the all-gather is the page-Adam's publish
   epilogue storing into every peer (hm_adam_main_ag) — no NCCL on the data
-  path; optionally pipelined over layer groups (``step_pipelined``);
+  path; optionally pipelined over layer groups (``step_pipelined``), or,
+  over a double-buffered fp32 state, ONE kernel for the reduce-scatter, the
+  update and the all-gather (the one-pass step);
 * ``ShardedPageStep`` (NCCL baseline): the 16-bit pools are laid out
   bucket-major, rank-major inside a bucket (layout.py), so bucket b is ONE
   contiguous buffer and rank r's owned pages are its r-th block:
@@ -232,6 +234,12 @@ class FusedShardedPageStep:
     ``mode="nvls"`` uses the NVSwitch multicast address: the reduction
     happens in the switch (multimem.ld_reduce) and one store reaches every
     GPU (multimem.st).  The buffer's pools must come from ``symmetric_alloc``.
+
+    With a double-buffered MasterState (``double_buffered=True``) ``step``
+    is the ONE-PASS form: a single kernel pulls every rank's gradient of the
+    owned pages, reduces, updates into the other state copy and publishes
+    into every rank, speculatively; a flag merge then commits the applied
+    layers (hm_dp_onepass_update / _finalize / hm_dp_republish_rejected).
     """
 
     def __init__(self, buffer, masters, group=None, mode: str = "p2p"):
