@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--reduce-ctas", type=int, nargs="*", default=[])
     ap.add_argument("--ag-publish", type=int, nargs="*", default=[])
+    ap.add_argument("--onepass", action="store_true",
+                    help="time the one-pass DP kernel (hm_dp_onepass_update) over double-buffered state")
     ap.add_argument("--solo", action="store_true",
                     help="only GPU 0 launches (clean ncu counters: no peer traffic into GPU 0)")
     args = ap.parse_args()
@@ -70,7 +72,7 @@ def main():
     for r in range(n):
         dev = torch.device("cuda", r)
         with torch.cuda.device(dev):
-            specs, page, lay, buf, ms = build_state(bargs, dev, n, r)
+            specs, page, lay, buf, ms = build_state(bargs, dev, n, r, double_buffered=args.onepass)
             buf.accumulate_flat(owned_grad_flat(lay, args.dtype, dev, 7 + r), 0)
             L = len(specs)
             span = lay.elems16
@@ -125,6 +127,32 @@ def main():
                                     D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), arr(p_ptrs), n, None,
                                     buf._dt, hc, None, D.sptr(x["stream"])))
 
+    def onepass(x):
+        eng, buf, ms = x["ms"]._eng, x["buf"], x["ms"]
+        dgroups = eng.desc.table(x["groups"])
+        rt = eng.rt_scratch(x["L"], x["stream"])
+        bc, bc_len = ms._bias(hyper, range(x["L"]))
+        x["flags"].zero_()
+        D.check(lib.hm_adam_prologue(D.ptr(dgroups), x["L"], D.ptr(rt), hc, D.ptr(bc), bc_len, 0,
+                                     D.ptr(ms._steps_spec), None, None, None, 1, None, None,
+                                     D.sptr(x["stream"])))
+        D.check(lib.hm_dp_onepass_update(D.ptr(eng.desc.static(x["adam"])), len(x["adam"]), D.ptr(dgroups),
+                                         D.ptr(rt), D.ptr(ms._state_sel), x["lay"].elems_state,
+                                         arr([D.ptr(y["buf"].g16_pool) for y in ranks]), arr(p_ptrs), n,
+                                         buf._dt, D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool),
+                                         D.ptr(x["flags"]), hc, None, D.sptr(x["stream"])))
+
+    if args.onepass:
+        sync_all()
+        phase(onepass)
+        t = float(np.median([phase(onepass) for _ in range(max(1, args.reps))]))
+        lay = ranks[0]["lay"]
+        S = 2 * sum(lay.numels)
+        print(json.dumps({"probe": "nvlink_onepass", "gpus": n, "config": args.config, "onepass_ms": t,
+                          "link_bytes_per_direction": 2 * S * (n - 1) / n,
+                          "link_gbs": 2 * S * (n - 1) / n / (t / 1e3) / 1e9,
+                          "hbm_algorithmic_bytes_per_gpu": (2 + 24 + 2) * lay.owned_numel()}))
+        return
     sync_all()
     rs_ms, up_ms = [], []
     for _ in range(args.reps):
