@@ -243,6 +243,10 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
                 "ag_publish": ["per-thread stores", "bulk", "bulk"][args.ag_publish],
                 "kernels": ("RS(grad pages) -> check -> flag all-reduce -> prologue -> "
                             "page-Adam(bucket) || AG(bucket)") if not fused else
+                           ("barrier -> speculative prologue -> ONE kernel: pull every rank's gradient "
+                            "page + f32 reduce + page-Adam into the other state copy + store to every "
+                            "rank -> barrier -> flag merge/commit -> republish rejected -> barrier")
+                           if dp.one_pass else
                            ("barrier -> fused reduce-scatter+check over peer memory -> barrier -> "
                             "flag merge -> prologue -> page-Adam with all-gather epilogue -> barrier")},
         "roofline": {"bound": "nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
