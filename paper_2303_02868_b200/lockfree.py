@@ -692,6 +692,8 @@ class ParamBuffer(_Paged):
         self._applied_iter = [-1] * L
         self._prepub = [None] * L          # (token, buffer) of p16 pre-published by update_layer
         self._dirty: set[int] = set()      # slots handed over with their flag/norm not consumed
+        self._snaps: list[int] = []        # taken slots whose ledger sum is still to be read
+        self._snap_row = None              # (ring row, its address, stream) of those reads
         self._ledger_on = ledger
         self.ledger = ConservationLedger(L)
         if ledger:
@@ -715,6 +717,7 @@ class ParamBuffer(_Paged):
     def _ledger_flush(self) -> None:
         """Resolve every pending ledger entry from the device rows (one
         synchronisation), then recycle the rows."""
+        self._flush_snaps()
         if not self._ring_pos:
             return
         torch.cuda.synchronize(self.device)
@@ -723,6 +726,37 @@ class ParamBuffer(_Paged):
         self._ring[:self._ring_pos].zero_()
         torch.cuda.synchronize(self.device)   # rows are zero before any stream reuses them
         self._ring_pos = 0
+
+    def _defer_snap(self, fidx: int, layer: int, stream) -> None:
+        """record_take of a three-call ``take`` (lockfree.py:237): the slot's
+        running ledger sum is read later, by one launch for every take since
+        the last flush.  A handed-over slot's sum cannot change before the
+        flush: the flush runs before any accumulate launch (the only writer)
+        and before any ledger read."""
+        if self._snap_row is not None and self._snap_row[2].cuda_stream != stream.cuda_stream:
+            self._flush_snaps()
+        if self._snap_row is None:
+            row, rptr = self._ledger_row()
+            self._snap_row = (row, rptr, stream)
+        self.ledger._pend(self.ledger._consumed[layer], self._snap_row[0], 2 * len(self._snaps))
+        self._snaps.append(fidx)
+        if len(self._snaps) == self.num_layers:     # one ring row holds L (sum, flag) pairs
+            self._flush_snaps()
+
+    def _flush_snaps(self, stream=None) -> None:
+        """Launch the deferred take snapshots (snapshot + reset of each slot's
+        ledger sum); ``stream``, when it differs, waits for them."""
+        if not self._snaps:
+            return
+        _row, rptr, st = self._snap_row
+        slots = np.asarray(self._snaps, np.uint32)
+        self._snaps, self._snap_row = [], None
+        D.check(N.lib().hm_stats_take(D.ptr(self._eng.desc.table(slots, st)), len(slots), None, None,
+                                      D.ptr(self._lsum), rptr, D.sptr(st)))
+        if stream is not None and stream.cuda_stream != st.cuda_stream:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            stream.wait_event(ev)
 
     def _reset_dirty(self, slots, stream) -> None:
         """Reset the flag / norm / ledger sum of slots about to take a first
@@ -800,6 +834,7 @@ class ParamBuffer(_Paged):
     # -- writes -----------------------------------------------------------------
     def _k3(self, src, src_dt, chunks, modes, slots, layers, stream, iteration) -> None:
         """One accumulate launch (K3) + the host bookkeeping of its messages."""
+        self._flush_snaps(stream)
         self._reset_dirty([f for f, m in zip(slots, modes) if not m], stream)
         row = None
         if self._ledger_on:
@@ -907,11 +942,8 @@ class ParamBuffer(_Paged):
         self._cast(self.g16_pool[buf], self._dt, g, N.DT_F32,
                    self.layout.seg_chunks(layer, "16", reverse=True), st)
         fidx = buf * self.num_layers + layer
-        if self._ledger_on:   # record_take: snapshot + reset the running sum
-            row, rptr = self._ledger_row()
-            D.check(N.lib().hm_stats_take(D.ptr(self._eng.desc.table(np.array([fidx], np.uint32), st)), 1,
-                                          None, None, D.ptr(self._lsum), rptr, D.sptr(st)))
-            self._record_consumed([layer], row)
+        if self._ledger_on:   # record_take: snapshot + reset of the running sum, deferred
+            self._defer_snap(fidx, layer, st)
         # the reject flag and norm stay for an update_layer of this tensor;
         # otherwise they are reset before the slot's next first message
         self._dirty.add(fidx)
@@ -927,6 +959,7 @@ class ParamBuffer(_Paged):
         self._check_layer(layer)
         st = self._stream(stream)
         if clear:
+            self._flush_snaps(st)
             if self._pending[layer]:
                 fidx = self._gsel[layer] * self.num_layers + layer
                 row = rptr = None
@@ -994,6 +1027,7 @@ class UpdateTicket:
         self.buffer = buffer
         self.layers = list(layers)
         L, span = buffer.num_layers, buffer.layout.elems16
+        buffer._flush_snaps(buffer._stream())
         rows, self.counts, self.newest = [], [], []
         for l in self.layers:
             gbuf, count, new = buffer._hand_over(l)

@@ -7,7 +7,10 @@ step, so the sample is a size-independent check of the whole step:
     rounded once;
   * the owner's p32/m32/v32 of the page: bit-exact vs the oracle Adam;
   * every rank's published 16-bit page: the cast of the oracle's p32.
-DP_PIPE=1 runs the layer-group pipelined step (the N=2 default)."""
+DP_PIPE=1 runs the layer-group pipelined two-phase step; DP_PIPE=2 the
+one-pass kernel over a double-buffered state (bench.py's N=2 default),
+which never writes the reduced gradient back, so that check is skipped and
+the state is read from each layer's current copy."""
 import os
 import sys
 from pathlib import Path
@@ -45,13 +48,14 @@ def main():
     params = [torch.empty(n, device=dev).normal_(0, 0.02, generator=gen) for n in numels]
     buf = LF.ParamBuffer(params, dtype="bf16", page_bytes=page, device=dev, layout=lay,
                          pool_alloc=symmetric_alloc)
-    ms = LF.MasterState(params, page_bytes=page, device=dev, layout=lay)
+    mode = os.environ.get("DP_PIPE", "0")
+    ms = LF.MasterState(params, page_bytes=page, device=dev, layout=lay, double_buffered=mode == "2")
     dp = FusedShardedPageStep(buf, ms)
     total = sum(numels)
     buf.accumulate_flat(grad_flat(total, 100 + rank, dev), 0)
     gsel = buf._gsel[0]
     hyper = LF.AdamHyper(lr=1e-3)
-    if os.environ.get("DP_PIPE", "0") == "1":
+    if mode == "1":
         dp.step_pipelined(hyper, 8, reduce_ctas=128)
     else:
         dp.step(hyper)
@@ -80,14 +84,18 @@ def main():
         if not np.array_equal(p16[off16:off16 + s.n].view(torch.int16).cpu().numpy().view(np.uint16),
                               O.to16(rp, "bf16").view(np.uint16)):
             failures.append(f"layer{l} page{s.page}: published page differs")
-        if lay.owned(s):
+        if lay.owned(s) and mode != "2":
             got = buf.g16_pool[gsel][off16:off16 + s.n].view(torch.int16).cpu().numpy().view(np.uint16)
             if not np.array_equal(got, red16.view(np.uint16)):
                 failures.append(f"layer{l} page{s.page}: reduced gradient differs")
+        if lay.owned(s):
             so = lay.slot_state(s.page) * lay.E + s.off
-            for name, pool, want in (("p32", ms.p32_pool, rp), ("m32", ms.m32_pool, rm), ("v32", ms.v32_pool, rv)):
+            for name, pool, want in (("p32", ms._current(ms.p32_pool, l), rp), ("m32", ms._current(ms.m32_pool, l), rm),
+                                     ("v32", ms._current(ms.v32_pool, l), rv)):
                 if not np.array_equal(pool[so:so + s.n].cpu().numpy().view(np.uint32), want.view(np.uint32)):
                     failures.append(f"layer{l} page{s.page}: owned {name} differs")
+    if ms.steps != [1] * len(numels):
+        failures.append(f"steps after one applied step: {sorted(set(ms.steps))}")
     ok = torch.tensor([0 if failures else 1], device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if failures:

@@ -113,7 +113,7 @@ def test_lockfree_runner_with_dp_step(delay):
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
 
 
-@pytest.mark.parametrize("pipe", [0, 1])
+@pytest.mark.parametrize("pipe", [0, 1, 2])
 def test_dp_step_full_c2_sampled(pipe):
     """The fused DP step at the size bench.py measures (C2, 4 MiB pages),
     sampled pages bit-exact (tests/dp_fullsize_worker.py)."""

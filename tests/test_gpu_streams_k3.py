@@ -131,3 +131,46 @@ def test_three_call_fast_path_rejects_every_time(cuda):
     buf.accumulate(LF.GradMessage(0, torch.ones(4096, dtype=torch.float16, device="cuda"), 2))
     assert bool(ms.update_layer(0, gr, LF.AdamHyper()))
     assert ms.steps == [1, 0]
+
+
+def test_deferred_take_snapshots_across_streams(cuda):
+    """``take`` records the ledger's take sum (hiermem/lockfree.py:237) by a
+    deferred launch shared by every take since the last flush.  Takes on one
+    stream, accumulates on another (whose first message resets the slot the
+    snapshot reads), and a publish(clear=True) in between: every consumed
+    sum equals the f64 sum of the gradient the take returned, the counts
+    match and the ledger balances."""
+    rng = np.random.default_rng(11)
+    params = _params(3)
+    buf = LF.ParamBuffer(params, dtype="fp16", page_bytes=PAGE)
+    s_take, s_acc = torch.cuda.Stream(), torch.cuda.Stream()
+    want = [[] for _ in SIZES]
+    for it in range(5):
+        s_acc.wait_stream(s_take)          # the data dependency a caller owns (pages reused)
+        with torch.cuda.stream(s_acc):
+            for l, n in enumerate(SIZES):
+                for _ in range(1 + (l + it) % 2):
+                    g = torch.from_numpy(rng.normal(0, 1e-2, n).astype(np.float16)).cuda()
+                    buf.accumulate(LF.GradMessage(l, g, it))
+        s_take.wait_stream(s_acc)
+        for l in reversed(range(len(SIZES))):
+            if it == 2 and l == 3:
+                with torch.cuda.stream(s_take):
+                    got = buf.read(l)[1].float().sum(dtype=torch.float64)   # keep the stream busy
+                buf.publish(l, params[l], clear=True, stream=s_take)        # a clear-consume instead of a take
+                want[l].append(None)
+                continue
+            g, _c, _n = buf.take(l, stream=s_take)
+            with torch.cuda.stream(s_take):
+                want[l].append(g.double().sum())
+    torch.cuda.synchronize()
+    import math
+    consumed, produced = buf.ledger.consumed_sums, buf.ledger.produced_deltas
+    for l in range(len(SIZES)):
+        assert len(consumed[l]) == len(want[l])
+        for c, w in zip(consumed[l], want[l]):
+            if w is not None:
+                assert c == pytest.approx(float(w), rel=1e-6, abs=1e-9)
+        # conservation (lockfree.py:300-326): what was produced was consumed
+        assert math.fsum(produced[l]) == math.fsum(consumed[l]), l
+    assert buf.ledger.messages_consumed == buf.ledger.messages_accumulated
