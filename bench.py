@@ -426,9 +426,10 @@ def run_three_call(args, buf, ms, hyper, grads):
     tensors (hiermem/lockfree.py:755-769: take -> update_layer ->
     publish(clear=False), layers reversed), after the K3 accumulate — to set
     beside ``device_step`` (K3 + the fused sweep of the same work).  take
-    widens (6 B/param); update_layer reads the taken 16-bit pages in place and
-    pre-publishes (28 B); p32[l] unpacks (8 B); publish only flips: 42 B/param
-    + one K3 (4 B) and ~4 launches per layer."""
+    widens (6 B/param); update_layer reads the taken 16-bit pages in place,
+    pre-publishes and writes the new p32 as a tensor in ONE launch (28 + 4 B);
+    p32[l] hands that tensor out; publish only flips: 38 B/param + one K3
+    (4 B), two launches per layer (+ one batched ledger snapshot)."""
     import torch
     L = buf.num_layers
     P = sum(buf.layout.numels)
@@ -444,8 +445,8 @@ def run_three_call(args, buf, ms, hyper, grads):
     stream = torch.cuda.current_stream()
     t = _events(stream, step, args.three_call_steps)
     buf._ledger_flush()
-    return {"params_per_s": P / (t / 1e3), "ms": t, "bytes_per_param": 46,
-            "gbs": 46 * P / (t / 1e3) / 1e9,
+    return {"params_per_s": P / (t / 1e3), "ms": t, "bytes_per_param": 42,
+            "gbs": 42 * P / (t / 1e3) / 1e9,
             "api": "accumulate_flat + per layer (reversed): ParamBuffer.take -> MasterState.update_layer -> "
                    "ParamBuffer.publish(MasterState.p32[l], clear=False), torch tensors"}
 

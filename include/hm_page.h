@@ -216,6 +216,25 @@ int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_l
                  float* p32, float* m32, float* v32, void* p16, int p16_dtype,
                  const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream);
 
+/* MasterState.update_layer of ONE layer whose gradient is its taken 16-bit
+ * page buffer (the three-call path, hiermem/lockfree.py:155-165 after
+ * ParamBuffer.take :226-241), prologue fused: one launch.  group: ONE
+ * hm_group_launch row (device).  Each CTA derives the layer's reject flag
+ * (nonfinite[flag], nullable), step = steps[group] + 1, bias pair and clip
+ * scale (sumsq[flag], nullable) itself; the last CTA to retire writes
+ * steps[group] (applied only) and *applied.  done: a device word that is 0
+ * between launches (the kernel re-arms it; one per stream).  p_out/out_off
+ * (nullable, together): the new p32 of every chunk is also stored to
+ * p_out[out_off[chunk] + i] — the layer as a contiguous tensor, so
+ * MasterState.p32[layer] needs no unpack.  Requires n_chunks >= 1 and
+ * 16-bit g16/p16 of the same dtype. */
+int hm_adam_layer(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* group,
+                  const void* g16, int dtype, float* p32, float* m32, float* v32, void* p16,
+                  const hm_adam_hyper* hyper, const float* bc_table, int64_t bc_len,
+                  int32_t* steps, uint32_t* applied, const uint32_t* nonfinite,
+                  const double* sumsq, uint32_t* done, float* p_out, const uint64_t* out_off,
+                  void* stream);
+
 /* ---- data-parallel page collectives fused with compute (NVLink/NVSwitch) ---
  * Pools are symmetric buffers mapped into every rank (peer virtual addresses,
  * optionally one NVLS multicast address).  Ownership: page % N

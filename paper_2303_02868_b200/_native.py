@@ -98,6 +98,8 @@ SIGNATURES = {
                                 _P, _INT, _P, _P, _P]),
     "hm_adam_main": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT,
                             C.POINTER(AdamHyperC), _OPTS, _P]),
+    "hm_adam_layer": (_INT, [_P, _I64, _P, _P, _INT, _P, _P, _P, _P, C.POINTER(AdamHyperC), _P, _I64,
+                             _P, _P, _P, _P, _P, _P, _P, _P]),
     "hm_dp_reduce_check": (_INT, [_P, _INT, _P, _P, _INT, _P, _I64, _P, _P, _OPTS, _P]),
     "hm_dp_flags_merge": (_INT, [_P, _P, _INT, _INT, _P, _P, _P]),
     "hm_adam_main_ag": (_INT, [_P, _I64, _P, _P, _P, _INT, _P, _P, _P, _P, _INT, _P, _INT,

@@ -29,6 +29,14 @@ namespace {
 
 constexpr int kPrologueThreads = 1024;
 
+// Global-norm clip coefficient folded into the gradient scale (f64 norm of
+// the unscaled gradient, one f32 rounding), shared by both prologue forms.
+__device__ __forceinline__ float clip_gscale(const hm_adam_hyper& hyper, double total) {
+  const double norm = sqrt(total) * (double)hyper.inv_scale;
+  const double coef = norm > (double)hyper.max_norm ? (double)hyper.max_norm / (norm + 1e-6) : 1.0;
+  return __fmul_rn(hyper.inv_scale, (float)coef);
+}
+
 // Per-layer decision: reject flag, step advance, bias-correction lookup,
 // optional global grad-norm clip.  One CTA; deterministic reduction order.
 __global__ void __launch_bounds__(kPrologueThreads)
@@ -48,12 +56,7 @@ adam_prologue(const hm_group_launch* __restrict__ groups, int n_groups,
       if (nonfinite == nullptr || nonfinite[f] == 0) local += sumsq[f];
     }
     const double total = block_sum<kPrologueThreads>(local, red);
-    if (threadIdx.x == 0) {
-      // Norm of the unscaled gradient; clip coefficient as in common practice.
-      const double norm = sqrt(total) * (double)hyper.inv_scale;
-      const double coef = norm > (double)hyper.max_norm ? (double)hyper.max_norm / (norm + 1e-6) : 1.0;
-      s_gscale = __fmul_rn(hyper.inv_scale, (float)coef);
-    }
+    if (threadIdx.x == 0) s_gscale = clip_gscale(hyper, total);   // norm of the unscaled gradient
   } else if (threadIdx.x == 0) {
     s_gscale = hyper.inv_scale;
   }
@@ -146,14 +149,17 @@ __device__ __forceinline__ void publish1(void* p16, const PeerPtrs& peers, uint6
 
 // NT threads per 4096-element chunk: 256 (2 granules/thread, all 7 loads of
 // both issued up front) or 512 (1 granule/thread, more warps to hide latency).
-template <int GDT, int PDT, int PUB, int NT>
+// OUT: the new masters are also stored to a contiguous tensor (pout, at the
+// chunk's tensor offset oo) — MasterState.p32[l] without an unpack pass.
+template <int GDT, int PDT, int PUB, int NT, bool OUT = false>
 __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
                                            const hm_group_launch* __restrict__ groups,
                                            const hm_group_rt* __restrict__ rt,
                                            const void* __restrict__ g, float* __restrict__ p32,
                                            float* __restrict__ m32, float* __restrict__ v32,
                                            void* __restrict__ p16, const hm_adam_hyper& hyper,
-                                           const PeerPtrs& peers, char* mc) {
+                                           const PeerPtrs& peers, char* mc,
+                                           float* __restrict__ pout = nullptr, uint64_t oo = 0) {
   const hm_group_launch gl = groups[c.slot];
   const hm_group_rt r = rt[c.slot];
   const uint64_t go = c.g_off + gl.g_shift;
@@ -166,8 +172,12 @@ __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
 
   if (!r.apply) {
     // Rejected layer: state untouched; still publish the unchanged masters.
-    if constexpr (kPub) {
-      for (uint32_t i = tid; i < n; i += NT) publish1<PDT, PUB>(p16, peers, po + i, p32[so + i]);
+    if constexpr (kPub || OUT) {
+      for (uint32_t i = tid; i < n; i += NT) {
+        const float x = p32[so + i];
+        if constexpr (kPub) publish1<PDT, PUB>(p16, peers, po + i, x);
+        if constexpr (OUT) pout[oo + i] = x;
+      }
     }
     return;
   }
@@ -195,6 +205,7 @@ __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
     Raw8<GDT> graw[VPT];
     F8 pv[VPT], mv[VPT], vv[VPT];
     bool live[VPT];
+    const bool ovec = OUT && (oo & (kVec - 1)) == 0 && vec_base<HM_DT_F32>(pout);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const uint32_t e = (uint32_t)(k * NT + tid) * kVec;
@@ -217,6 +228,14 @@ __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
       store8<HM_DT_F32>(p32, so + e, pv[k]);
       store8<HM_DT_F32>(m32, so + e, mv[k]);
       store8<HM_DT_F32>(v32, so + e, vv[k]);
+      if constexpr (OUT) {
+        if (ovec) {
+          store8<HM_DT_F32>(pout, oo + e, pv[k]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) pout[oo + e + j] = pv[k].v[j];
+        }
+      }
       if constexpr (is_bulk<PUB>()) {
         using T = typename Elem<PDT>::T;
         uint4 u;
@@ -258,8 +277,64 @@ __device__ __forceinline__ void adam_chunk(const hm_adam_chunk& c,
       m32[so + i] = m;
       v32[so + i] = v;
       if constexpr (kPub) publish1<PDT, PUB>(p16, peers, po + i, p);
+      if constexpr (OUT) pout[oo + i] = p;
     }
   }
+}
+
+// update_layer of ONE layer from its 16-bit pages in ONE launch (the three-
+// call path, hiermem/lockfree.py:155-165): each CTA derives the layer's
+// runtime record itself — reject flag, step + 1, bias pair, clip scale, as
+// adam_prologue does for a multi-layer launch — and the last CTA to retire
+// commits the step (applied layers only) and the applied word.  Every CTA
+// reads steps[] before its arrival on `done`, so the commit never races a
+// read; the last CTA re-arms `done` for the stream's next launch.
+template <int GDT, int PDT, bool OUT>
+__global__ void __launch_bounds__(kThreads)
+adam_layer(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ group,
+           const void* __restrict__ g, float* __restrict__ p32, float* __restrict__ m32,
+           float* __restrict__ v32, void* __restrict__ p16, hm_adam_hyper hyper,
+           const float* __restrict__ bc_table, int64_t bc_len, int32_t* __restrict__ steps,
+           uint32_t* __restrict__ applied, const uint32_t* __restrict__ nonfinite,
+           const double* __restrict__ sumsq, uint32_t* __restrict__ done, float* __restrict__ pout,
+           const uint64_t* __restrict__ out_off) {
+  __shared__ hm_group_rt s_rt;
+  __shared__ int32_t s_step;
+  if (threadIdx.x == 0) {
+    const hm_group_launch gl = group[0];
+    const bool finite = nonfinite == nullptr || nonfinite[gl.flag] == 0;
+    int64_t st = (int64_t)steps[gl.group] + 1;
+    s_step = (int32_t)st;
+    if (st >= bc_len) st = bc_len - 1;   // the table saturates at 1.0f
+    hm_group_rt r;
+    r.bc1 = bc_table[2 * st];
+    r.bc2 = bc_table[2 * st + 1];
+    r.gscale = hyper.max_norm > 0.f && sumsq != nullptr ? clip_gscale(hyper, finite ? sumsq[gl.flag] : 0.0)
+                                                         : hyper.inv_scale;
+    r.apply = finite ? 1u : 0u;
+    s_rt = r;
+  }
+  __syncthreads();
+  adam_chunk<GDT, PDT, kPubLocal, kThreads, OUT>(chunks[blockIdx.x], group, &s_rt, g, p32, m32, v32, p16,
+                                                 hyper, PeerPtrs{}, nullptr, pout,
+                                                 OUT ? out_off[blockIdx.x] : 0);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      if (s_rt.apply) steps[group[0].group] = s_step;
+      *applied = s_rt.apply;
+      *done = 0u;
+    }
+  }
+}
+
+using AdamLayerFn = void (*)(const hm_adam_chunk*, const hm_group_launch*, const void*, float*, float*,
+                             float*, void*, hm_adam_hyper, const float*, int64_t, int32_t*, uint32_t*,
+                             const uint32_t*, const double*, uint32_t*, float*, const uint64_t*);
+
+template <int DT>
+AdamLayerFn pick_adam_layer_dt(bool out) {
+  return out ? adam_layer<DT, DT, true> : adam_layer<DT, DT, false>;
 }
 
 template <int GDT, int PDT, int PUB = kPubLocal, int NT = kThreads>
@@ -410,6 +485,31 @@ extern "C" int hm_adam_main(const hm_adam_chunk* chunks, int64_t n_chunks,
   hm::PeerPtrs none{};
   fn<<<(unsigned)n_chunks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
       chunks, groups, rt, g, p32, m32, v32, p16, *hyper, none, nullptr);
+  HM_CUDA_CHECK_LAUNCH();
+  return HM_OK;
+}
+
+extern "C" int hm_adam_layer(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* group,
+                             const void* g16, int dtype, float* p32, float* m32, float* v32, void* p16,
+                             const hm_adam_hyper* hyper, const float* bc_table, int64_t bc_len,
+                             int32_t* steps, uint32_t* applied, const uint32_t* nonfinite,
+                             const double* sumsq, uint32_t* done, float* p_out, const uint64_t* out_off,
+                             void* stream) {
+  if (!hyper || !bc_table || bc_len < 1)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_layer: missing hyper/bc_table");
+  if (n_chunks <= 0 || n_chunks > 0x7fffffffLL)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_layer: bad chunk count %lld (a layer without "
+                        "pages here takes hm_adam_step)", (long long)n_chunks);
+  if (dtype != HM_DT_BF16 && dtype != HM_DT_F16)
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_layer: 16-bit pages only, got dtype %d", dtype);
+  if ((p_out == nullptr) != (out_off == nullptr))
+    return hm_set_error(HM_ERR_INVALID, "hm_adam_layer: p_out and out_off go together");
+  HM_REQUIRE_PTRS("hm_adam_layer", chunks, group, g16, p32, m32, v32, p16, steps, applied, done);
+  hm::AdamLayerFn fn = dtype == HM_DT_BF16 ? hm::pick_adam_layer_dt<HM_DT_BF16>(p_out != nullptr)
+                                           : hm::pick_adam_layer_dt<HM_DT_F16>(p_out != nullptr);
+  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      chunks, group, g16, p32, m32, v32, p16, *hyper, bc_table, bc_len, steps, applied, nonfinite, sumsq,
+      done, p_out, out_off);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }

@@ -152,6 +152,14 @@ class PageLayout:
         reverse=False: src = tensor, dst = pool (pack); True: unpack."""
         return _seg_chunks(self, layer, pool, owned_only, slot, reverse)
 
+    def adam_tensor_pos(self, layer: int) -> np.ndarray:
+        """uint64 tensor offset of every unit of ``adam_chunks([layer])``
+        (owned units, same order): where hm_adam_layer stores the new p32."""
+        cache = self.__dict__.setdefault("_tpos_cache", {})
+        if layer not in cache:
+            cache[layer] = _unit_arrays(self, layer, True)[2].astype(np.uint64)
+        return cache[layer]
+
     def pool_chunks(self, layers, pool: str = "16", owned_only: bool = True) -> np.ndarray:
         """hm_seg_chunk over pool segments with src == dst == pool offsets and
         slot = index in ``layers`` (reductions / casts done in place)."""

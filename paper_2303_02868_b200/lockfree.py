@@ -45,7 +45,9 @@ from .pagemem import PAGE_BYTES_DEFAULT
 class AdamHyper:
     """hiermem/lockfree.py:37-42, plus two B200 additions that are exact
     identities at their defaults: ``inv_scale`` (loss-scale unscale, x*1.0f)
-    and ``max_norm`` (global grad-norm clip, <= 0 disables)."""
+    and ``max_norm`` (grad-norm clip, <= 0 disables; the norm is over the
+    layers of one update: a sweep's or DP step's layers, the one layer of an
+    ``update_layer``, the tensor of an ``apply_update``)."""
 
     lr: float = 0.01
     beta1: float = 0.9
@@ -232,6 +234,8 @@ class _StreamScratch:
         with torch.cuda.stream(stream):
             self.rt = torch.empty(64 * N.GROUP_RT_BYTES, dtype=torch.uint8, device=device)
             self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+            self.done = torch.zeros(1, dtype=torch.int32, device=device)   # hm_adam_layer's arrival count
+            self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)  # update_layer's clip norm
 
     def rt_for(self, n_groups: int) -> torch.Tensor:
         need = max(1, n_groups) * N.GROUP_RT_BYTES
@@ -368,11 +372,12 @@ def apply_update(p32, m32, v32, grad, hyper: AdamHyper, step: int, *, stream=Non
                            float(np.float32(1.0 - hyper.beta2 ** step))], dtype=torch.float32, device=device)
         flag = torch.zeros(1, dtype=torch.int32, device=device)
         applied = torch.zeros(1, dtype=torch.int32, device=device)
+        sumsq = torch.zeros(1, dtype=torch.float64, device=device) if hyper.max_norm > 0 else None
     cc = D.contiguous_chunks_cached(n)
     D.check(N.lib().hm_reduce_stats(D.ptr(g), D.DT_OF_TORCH[g.dtype], D.ptr(eng.desc.static(cc)), len(cc),
-                                     D.ptr(flag), None, None, D.sptr(st)))
+                                     D.ptr(flag), None, D.addr(sumsq), D.sptr(st)))
     adam_launch(eng, D.contiguous_adam_chunks(n), _group_rows([(0, 0, 0, 0)]), g, D.DT_OF_TORCH[g.dtype],
-                p, m, v, None, 0, hyper, bc, 1, int(step), None, applied, flag, None, True, st,
+                p, m, v, None, 0, hyper, bc, 1, int(step), None, applied, flag, sumsq, True, st,
                 static_chunks=False)
     with D.on(st):
         if not bool(applied.item()):
@@ -491,7 +496,10 @@ class MasterState(_Paged):
                 self._state_sel = torch.zeros(self.num_layers, dtype=torch.int32, device=self.device)
                 self._steps_spec = torch.zeros_like(self._steps)
         self._step_bound = [0] * self.num_layers
-        self._prepub = [None] * self.num_layers   # (buffer ref, token) of a pre-published p16
+        # per layer, after a fast update_layer: (buffer ref, token of the
+        # pre-published p16, the new p32 as a tensor or None, its stream)
+        self._prepub = [None] * self.num_layers
+        self._pout_layer = None
         for l, p in enumerate(params):
             self._pack_p32(l, p, st)
 
@@ -527,13 +535,19 @@ class MasterState(_Paged):
         return [int(x) for x in self._steps.cpu().tolist()]
 
     def _p32_of(self, layer):
-        out = self._unpack(self._current(self.p32_pool, layer), layer)
-        if isinstance(out, torch.Tensor) and self._prepub[layer] is not None:
+        pre = self._prepub[layer]
+        if pre is not None and pre[2] is not None and pre[3].cuda_stream == self._stream().cuda_stream:
+            # the fast update_layer also wrote the new masters as a
+            # contiguous tensor: handed out once, later reads unpack
+            out = self._out(pre[2], layer)
+            self._prepub[layer] = pre = (pre[0], pre[1], None, None)
+        else:
+            out = self._unpack(self._current(self.p32_pool, layer), layer)
+        if isinstance(out, torch.Tensor) and pre is not None:
             # the fast update_layer already cast these values into the
             # buffer's inactive publish pages: publish() of this unmodified
             # tensor only has to flip the record
-            bref, token = self._prepub[layer]
-            out._hm_prepub = (bref, token, layer, out._version)
+            out._hm_prepub = (pre[0], pre[1], layer, out._version)
         return out
 
     def _pack_p32(self, layer, value, stream=None):
@@ -594,39 +608,65 @@ class MasterState(_Paged):
         if g.numel() != n:
             raise ProtocolError(f"gradient has {g.numel()} elements, layer {layer} has {n}")
         eng = self._eng
-        flag = eng.scratch(st).flag
+        sc = eng.scratch(st)
+        flag, sumsq = sc.flag, (sc.sumsq if hyper.max_norm > 0 else None)   # clip: the layer's own norm
         with D.on(st):
             flag.zero_()
+            if sumsq is not None:
+                sumsq.zero_()
         cc = D.contiguous_chunks_cached(n)
         D.check(N.lib().hm_reduce_stats(D.ptr(g), D.DT_OF_TORCH[g.dtype], D.ptr(eng.desc.static(cc)),
-                                         len(cc), D.ptr(flag), None, None, D.sptr(st)))
+                                         len(cc), D.ptr(flag), None, D.addr(sumsq), D.sptr(st)))
         bc, bc_len = self._bias(hyper, [layer])
         with D.on(st):
             out = torch.empty(1, dtype=torch.int32, device=self.device)
         adam_launch(eng, self.layout.adam_chunks([layer], "tensor"), _group_rows([(0, 0, 0, 0)]),
                     g, D.DT_OF_TORCH[g.dtype], self.p32_pool, self.m32_pool, self.v32_pool, None, 0,
-                    hyper, bc, bc_len, 0, D.ptr(self._steps) + 4 * layer, out, flag, None, True, st)
+                    hyper, bc, bc_len, 0, D.ptr(self._steps) + 4 * layer, out, flag, sumsq, True, st)
         return self._applied_result(out, st)
 
     def _update_from_pages(self, buf, gbuf: int, layer: int, hyper, st):
         L, span = buf.num_layers, buf.layout.elems16
+        lay, eng = self.layout, self._eng
         nxt = buf._psel[layer] ^ 1
         fidx = gbuf * L + layer
+        chunks = lay.adam_chunks([layer], "pool")
         bc, bc_len = self._bias(hyper, [layer])
-        with D.on(st):
-            out = torch.empty(1, dtype=torch.int32, device=self.device)
         # group 0 of the launch = this layer: steps[] is addressed at the
         # layer's counter, applied[] is the per-call result word
-        adam_launch(self._eng, self.layout.adam_chunks([layer], "pool"),
-                    _group_rows([(gbuf * span, nxt * span, 0, fidx)]), buf.g16_pool, buf._dt,
-                    self.p32_pool, self.m32_pool, self.v32_pool, buf.p16_pool, buf._dt, hyper, bc, bc_len,
-                    0, D.ptr(self._steps) + 4 * layer, out, buf._flags, buf._sumsq, False, st)
+        rows = _group_rows([(gbuf * span, nxt * span, 0, fidx)])
+        p_out = None
+        with D.on(st):
+            out = torch.empty(1, dtype=torch.int32, device=self.device)
+            if lay.world_size == 1:
+                p_out = torch.empty(lay.numels[layer], dtype=torch.float32, device=self.device)
+        if len(chunks):
+            # ONE launch (prologue fused); the new masters also land in p_out
+            # for the p32[layer] read that follows in the reference loop
+            D.check(N.lib().hm_adam_layer(
+                D.ptr(eng.desc.static(chunks)), len(chunks), D.ptr(eng.desc.table(rows, st)),
+                D.ptr(buf.g16_pool), buf._dt, D.ptr(self.p32_pool), D.ptr(self.m32_pool),
+                D.ptr(self.v32_pool), D.ptr(buf.p16_pool), D.hyper_c(hyper), D.ptr(bc), bc_len,
+                D.ptr(self._steps) + 4 * layer, D.ptr(out), D.ptr(buf._flags), D.ptr(buf._sumsq),
+                D.ptr(eng.scratch(st).done), D.ptr(p_out) if p_out is not None else None,
+                D.ptr(eng.desc.static(lay.adam_tensor_pos(layer))) if p_out is not None else None,
+                D.sptr(st)))
+        else:   # no owned page of this layer on this rank: the step bookkeeping only
+            p_out = None
+            adam_launch(eng, chunks, rows, buf.g16_pool, buf._dt, self.p32_pool, self.m32_pool,
+                        self.v32_pool, buf.p16_pool, buf._dt, hyper, bc, bc_len, 0,
+                        D.ptr(self._steps) + 4 * layer, out, buf._flags, buf._sumsq, False, st)
         # the flag is read, not consumed: a second update_layer of the same
         # tensor must see the same verdict (the reference re-checks, :133);
         # the slot stays marked for a reset before its next first message
         token = object()
         buf._prepub[layer] = (token, nxt)
-        self._prepub[layer] = (weakref.ref(buf), token)
+        # at most one unclaimed p_out is kept (memory: one layer)
+        if self._pout_layer is not None and self._prepub[self._pout_layer] is not None:
+            q = self._prepub[self._pout_layer]
+            self._prepub[self._pout_layer] = (q[0], q[1], None, None)
+        self._prepub[layer] = (weakref.ref(buf), token, p_out, st if p_out is not None else None)
+        self._pout_layer = layer if p_out is not None else None
         return self._applied_result(out, st)
 
     def _applied_result(self, out: torch.Tensor, st):
@@ -1075,6 +1115,10 @@ def update_prologue(ticket: UpdateTicket, masters, hyper, stream, *, flags=None,
     which must run on ``stream`` (the rt scratch is the stream's)."""
     b = ticket.buffer
     eng = masters._eng
+    pre = getattr(masters, "_prepub", None)
+    if pre is not None:    # a fast update_layer's pre-published results are stale now
+        for l in ticket.layers:
+            pre[l] = None
     dgroups = eng.desc.table(ticket.groups, stream)
     rt = eng.rt_scratch(len(ticket.groups), stream)
     bc, bc_len = masters._bias(hyper, ticket.layers)

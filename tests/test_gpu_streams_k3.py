@@ -174,3 +174,54 @@ def test_deferred_take_snapshots_across_streams(cuda):
         # conservation (lockfree.py:300-326): what was produced was consumed
         assert math.fsum(produced[l]) == math.fsum(consumed[l]), l
     assert buf.ledger.messages_consumed == buf.ledger.messages_accumulated
+
+
+def _bits(t):
+    return t.detach().contiguous().view(torch.int32).cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("max_norm", [0.0, 0.05])
+def test_fused_layer_update_matches_generic_path(cuda, dtype, max_norm):
+    """The three-call update_layer on a taken tensor is ONE hm_adam_layer
+    launch (prologue fused; the new masters also written as the contiguous
+    tensor p32[l] hands out once).  It must equal the generic update_layer
+    (prologue + main kernel over the f32 tensor, unpack on read): bit-exact
+    without clipping, within f32 rounding of the clip coefficient with it
+    (the two paths sum the squared norm in different orders).  Covers
+    layers whose tensor offsets are not 8-aligned (SIZES), a rejected
+    layer, a second p32 read (unpacked), and a sweep after an unclaimed
+    fused update (the stale tensor must not be handed out)."""
+    rng = np.random.default_rng(21)
+    params = _params(5)
+    hyper = LF.AdamHyper(lr=1e-3, max_norm=max_norm)
+    buf = LF.ParamBuffer(params, dtype=dtype, page_bytes=PAGE)
+    fast, slow = LF.MasterState(params, page_bytes=PAGE), LF.MasterState(params, page_bytes=PAGE)
+    t16 = torch.float16 if dtype == "fp16" else torch.bfloat16
+    same = (lambda a, b: np.array_equal(_bits(a), _bits(b))) if max_norm == 0 else \
+        (lambda a, b: torch.allclose(a, b, rtol=2e-6, atol=1e-9))
+    for it in range(4):
+        for l, n in enumerate(SIZES):
+            g = torch.from_numpy(rng.normal(0, 1e-2, n).astype(np.float32)).cuda()
+            if it == 2 and l == 3:
+                g[n // 3] = float("inf")
+            buf.accumulate(LF.GradMessage(l, g.to(t16), it))
+        for l in reversed(range(len(SIZES))):
+            gr, _c, newest = buf.take(l)
+            ok_f = fast.update_layer(l, gr, hyper)
+            ok_s = slow.update_layer(l, gr.clone(), hyper)
+            assert bool(ok_f) == bool(ok_s) == (not (it == 2 and l == 3)), (it, l)
+            pf, pf2, ps = fast.p32[l], fast.p32[l], slow.p32[l]
+            assert same(pf, ps) and np.array_equal(_bits(pf), _bits(pf2)), (it, l)
+            buf.publish(l, pf, applied_iter=newest, clear=False)
+    assert fast.steps == slow.steps
+    for l in range(len(SIZES)):
+        assert same(fast.m32[l], slow.m32[l]) and same(fast.v32[l], slow.v32[l]), l
+    # an unclaimed fused result, then a sweep of the same layer: p32 reads the new state
+    buf.accumulate(LF.GradMessage(0, torch.ones(SIZES[0], dtype=t16, device="cuda") * 1e-2, 9))
+    gr, _c, _n = buf.take(0)
+    fast.update_layer(0, gr, hyper)
+    buf.accumulate(LF.GradMessage(0, torch.ones(SIZES[0], dtype=t16, device="cuda") * 1e-2, 10))
+    LF.sweep(buf, fast, hyper, layers=[0])
+    p = fast.p32[0]
+    assert np.array_equal(_bits(p), _bits(fast._unpack(fast.p32_pool, 0)))
