@@ -144,18 +144,23 @@ __global__ void onepass_finalize_kernel(PeerPtrs flag_peers, int n_layers, int32
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads)
-republish_kernel(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __restrict__ groups,
-                 const uint32_t* __restrict__ applied, const uint32_t* __restrict__ state_sel, uint64_t es,
-                 const float* __restrict__ p32, PeerPtrs ppeers) {
-  const hm_adam_chunk c = chunks[blockIdx.x];
-  const hm_group_launch gl = groups[c.slot];
-  if (applied[gl.group]) return;   // uniform: the common case exits at once
-  const uint64_t sr = c.s_off + (uint64_t)state_sel[gl.group] * es, po = c.p_off + gl.p_shift;
-  for (uint32_t i = threadIdx.x; i < c.n; i += kThreads) {
-    const float p = p32[sr + i];
+republish_kernel(const hm_adam_chunk* __restrict__ chunks, int n_chunks,
+                 const hm_group_launch* __restrict__ groups, const uint32_t* __restrict__ applied,
+                 const uint32_t* __restrict__ state_sel, uint64_t es, const float* __restrict__ p32,
+                 PeerPtrs ppeers) {
+  // a persistent grid striding over the chunks: the common case (nothing
+  // rejected) is one descriptor + one flag read per chunk, not one CTA each
+  for (int k = blockIdx.x; k < n_chunks; k += gridDim.x) {
+    const hm_adam_chunk c = chunks[k];
+    const hm_group_launch gl = groups[c.slot];
+    if (applied[gl.group]) continue;   // uniform per chunk
+    const uint64_t sr = c.s_off + (uint64_t)state_sel[gl.group] * es, po = c.p_off + gl.p_shift;
+    for (uint32_t i = threadIdx.x; i < c.n; i += kThreads) {
+      const float p = p32[sr + i];
 #pragma unroll
-    for (int q = 0; q < kMaxPeers; ++q)
-      if (q < ppeers.n) store1<DT>(reinterpret_cast<void*>(ppeers.p[q]), po + i, p);
+      for (int q = 0; q < kMaxPeers; ++q)
+        if (q < ppeers.n) store1<DT>(reinterpret_cast<void*>(ppeers.p[q]), po + i, p);
+    }
   }
 }
 
@@ -227,8 +232,12 @@ int hm_dp_republish_rejected(const hm_adam_chunk* chunks, int64_t n_chunks, cons
   if (n_chunks == 0) return HM_OK;
   HM_REQUIRE_PTRS("hm_dp_republish_rejected", chunks, groups, applied, state_sel, p32);
   auto fn = dtype == HM_DT_BF16 ? hm::republish_kernel<HM_DT_BF16> : hm::republish_kernel<HM_DT_F16>;
-  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      chunks, groups, applied, state_sel, (uint64_t)state_elems, p32, pp);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = n_chunks < 8 * sms ? n_chunks : 8 * sms;   // 8 resident CTAs per SM
+  fn<<<(unsigned)grid, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      chunks, (int)n_chunks, groups, applied, state_sel, (uint64_t)state_elems, p32, pp);
   HM_CUDA_CHECK_LAUNCH();
   return HM_OK;
 }
