@@ -10,8 +10,9 @@ take -> update_layer -> publish fast path, and the DP kernels (reduce-
 scatter in both load widths, as a persistent grid and 8-wide; flag merge;
 update with the per-thread and the staged bulk-copy all-gather epilogue and
 the persistent update grid) with the local pools standing in for every
-peer — and every guard band must be bit-identical afterwards, and the
-results equal to the plain sweep's.
+peer, and the one-launch layer update with its contiguous p32 output — and
+every guard band must be bit-identical afterwards, and the results equal
+to the plain sweep's.
 """
 import ctypes as C
 
@@ -103,6 +104,30 @@ def _dp_self(buf, ms, hyper):
                                     o, D.sptr(st)))
 
 
+def _layer_self(buf, ms, hyper, guard):
+    """hm_adam_layer (the one-launch update_layer) of every layer straight
+    through the C-ABI, its contiguous p32 output guarded too; every output
+    must equal the pool it mirrors."""
+    lib, eng, lay = N.lib(), ms._eng, buf.layout
+    st = torch.cuda.current_stream()
+    L, span = buf.num_layers, lay.elems16
+    for l in range(L):
+        alloc = guard if guard is not None else (lambda shape, dt, dev: torch.empty(*shape, dtype=dt, device=dev))
+        pout = alloc((lay.numels[l],), torch.float32, buf.device)
+        out = torch.zeros(1, dtype=torch.int32, device=buf.device)
+        rows = np.zeros(1, dtype=N.GROUP_LAUNCH)
+        rows[0] = (buf._gsel[l] * span, (buf._psel[l] ^ 1) * span, 0, buf._gsel[l] * L + l)
+        chunks = lay.adam_chunks([l], "pool")
+        bc, bc_len = ms._bias(hyper, [l])
+        D.check(lib.hm_adam_layer(D.ptr(eng.desc.static(chunks)), len(chunks), D.ptr(eng.desc.table(rows, st)),
+                                  D.ptr(buf.g16_pool), buf._dt, D.ptr(ms.p32_pool), D.ptr(ms.m32_pool),
+                                  D.ptr(ms.v32_pool), D.ptr(buf.p16_pool), D.hyper_c(hyper), D.ptr(bc), bc_len,
+                                  D.ptr(ms._steps) + 4 * l, D.ptr(out), D.ptr(buf._flags), D.ptr(buf._sumsq),
+                                  D.ptr(eng.scratch(st).done), D.ptr(pout),
+                                  D.ptr(eng.desc.static(lay.adam_tensor_pos(l))), D.sptr(st)))
+        assert torch.equal(pout.view(torch.int32), ms._unpack(ms.p32_pool, l).view(torch.int32)), l
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 def test_no_kernel_writes_outside_its_pools(cuda, dtype):
     hyper = LF.AdamHyper(lr=1e-3)
@@ -125,6 +150,7 @@ def test_no_kernel_writes_outside_its_pools(cuda, dtype):
         LF.sweep(buf, ms, hyper)
         buf.accumulate_flat(flat, 4)
         _dp_self(buf, ms, hyper)
+        _layer_self(buf, ms, hyper, guard if g is not None else None)
         torch.cuda.synchronize()
         results.append((ms.p32_pool.clone(), buf.p16_pool.clone()))
     assert guard.intact(), "a kernel wrote into a guard band"
