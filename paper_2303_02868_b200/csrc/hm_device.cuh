@@ -232,6 +232,35 @@ __device__ __forceinline__ double block_sum(double x, double* smem) {
   return r;  // valid in thread 0
 }
 
+// ---- programmatic dependent launch -----------------------------------------
+// A kernel launched by launch_pdl may become resident while the previous
+// kernel of the stream drains.  pdl_enter, its first statement, lets its own
+// successor do the same and then waits for the previous grid to complete
+// with its memory visible — before any data is touched, so stream order is
+// unchanged and only the launch latency between the two kernels is hidden
+// (the three-call path issues ~2 small launches per layer).  Both
+// instructions are no-ops in a normal launch.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t stream,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 }  // namespace hm
 
 #define HM_CUDA_CHECK_LAUNCH()                                                          \

@@ -300,6 +300,7 @@ adam_layer(const hm_adam_chunk* __restrict__ chunks, const hm_group_launch* __re
            const uint64_t* __restrict__ out_off) {
   __shared__ hm_group_rt s_rt;
   __shared__ int32_t s_step;
+  pdl_enter();
   if (threadIdx.x == 0) {
     const hm_group_launch gl = group[0];
     const bool finite = nonfinite == nullptr || nonfinite[gl.flag] == 0;
@@ -507,10 +508,10 @@ extern "C" int hm_adam_layer(const hm_adam_chunk* chunks, int64_t n_chunks, cons
   HM_REQUIRE_PTRS("hm_adam_layer", chunks, group, g16, p32, m32, v32, p16, steps, applied, done);
   hm::AdamLayerFn fn = dtype == HM_DT_BF16 ? hm::pick_adam_layer_dt<HM_DT_BF16>(p_out != nullptr)
                                            : hm::pick_adam_layer_dt<HM_DT_F16>(p_out != nullptr);
-  fn<<<(unsigned)n_chunks, hm::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      chunks, group, g16, p32, m32, v32, p16, *hyper, bc_table, bc_len, steps, applied, nonfinite, sumsq,
-      done, p_out, out_off);
-  HM_CUDA_CHECK_LAUNCH();
+  const cudaError_t e = hm::launch_pdl(fn, (unsigned)n_chunks, hm::kThreads, static_cast<cudaStream_t>(stream),
+                                       chunks, group, g16, p32, m32, v32, p16, *hyper, bc_table, bc_len, steps,
+                                       applied, nonfinite, sumsq, done, p_out, out_off);
+  if (e != cudaSuccess) return hm_set_error(HM_ERR_CUDA, "hm_adam_layer: %s", cudaGetErrorString(e));
   return HM_OK;
 }
 

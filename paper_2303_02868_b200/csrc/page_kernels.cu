@@ -292,6 +292,7 @@ template <int SDT, int DDT>
 __global__ void __launch_bounds__(kSegThreads)
 cast_kernel(const hm_seg_chunk* __restrict__ chunks, const void* __restrict__ src,
             void* __restrict__ dst) {
+  pdl_enter();
   const hm_seg_chunk c = chunks[blockIdx.x];
   const int tid = threadIdx.x;
   const bool vec = ((c.src_off | c.dst_off | (uint64_t)c.n) & (kVec - 1)) == 0 &&
@@ -550,8 +551,9 @@ int hm_cast(const void* src, int src_dtype, void* dst, int dst_dtype, const hm_s
   if (!fn) return hm_set_error(HM_ERR_INVALID, "hm_cast: unsupported dtypes %d -> %d", src_dtype, dst_dtype);
   if (n_chunks == 0) return HM_OK;
   HM_REQUIRE_PTRS("hm_cast", src, dst, chunks);
-  fn<<<(unsigned)n_chunks, hm::kSegThreads, 0, static_cast<cudaStream_t>(stream)>>>(chunks, src, dst);
-  HM_CUDA_CHECK_LAUNCH();
+  const cudaError_t e = hm::launch_pdl(fn, (unsigned)n_chunks, hm::kSegThreads, static_cast<cudaStream_t>(stream),
+                                       chunks, src, dst);
+  if (e != cudaSuccess) return hm_set_error(HM_ERR_CUDA, "hm_cast: %s", cudaGetErrorString(e));
   return HM_OK;
 }
 
