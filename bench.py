@@ -543,6 +543,9 @@ def main():
                     help="fused P2P DP step as ONE kernel over a double-buffered fp32 state "
                          "(reduce-scatter + update + all-gather, commit after a flag merge); "
                          "-1 = auto (on at N=2, where it wins; profiles/r2_bench.md)")
+    ap.add_argument("--dp-push", type=int, default=-1, choices=[-1, 0, 1],
+                    help="one-pass DP step: 1 = push form (every rank stores the non-owned gradient into the "
+                         "owner's receive pool), 0 = pull form, -1 = the measured policy")
     ap.add_argument("--dp-mode", default="p2p", choices=["nccl", "p2p", "nvls"],
                     help="N>1 collectives: NCCL RS/AG, or fused kernels over NVLink peer memory "
                          "(p2p) / NVSwitch multicast (nvls)")

@@ -291,6 +291,25 @@ int hm_dp_onepass_update(const hm_adam_chunk* chunks, int64_t n_chunks, const hm
                          const uint64_t* peer_g16, const uint64_t* peer_p16, int n_peers, int dtype,
                          float* p32, float* m32, float* v32, uint32_t* nonfinite,
                          const hm_adam_hyper* hyper, const hm_launch_opts* opts, void* stream);
+/* Push form of the one-pass step's gradient exchange (N >= 4): every rank
+ * stores the gradient of the pages it does NOT own into the owner's receive
+ * pool (NVLink writes, no read requests).  chunks: src_off = element offset
+ * in g16_local (this rank's active gradient buffer), dst_off = the page's
+ * state-slot offset on its owner, slot = owner rank; recv_ptrs: DEVICE array
+ * of every rank's receive-pool address; element dst_base (= rank x
+ * slot_elems) selects this rank's slot there. */
+int hm_dp_push_grad(const hm_seg_chunk* chunks, int64_t n_chunks, const void* g16_local,
+                    const uint64_t* recv_ptrs, int64_t dst_base, void* stream);
+/* hm_dp_onepass_update reading rank q's share of an owned chunk from
+ * g16_local (q == self_rank, at the chunk's gradient offset) or from
+ * recv_local + q x slot_elems + the chunk's state offset (after
+ * hm_dp_push_grad and a barrier): same rank-order f32 sum, same bits. */
+int hm_dp_onepass_recv_update(const hm_adam_chunk* chunks, int64_t n_chunks, const hm_group_launch* groups,
+                              const hm_group_rt* rt, const uint32_t* state_sel, int64_t state_elems,
+                              const void* g16_local, const void* recv_local, int64_t slot_elems, int self_rank,
+                              int n_ranks, const uint64_t* peer_p16, int n_peers, int dtype, float* p32,
+                              float* m32, float* v32, uint32_t* nonfinite, const hm_adam_hyper* hyper,
+                              void* stream);
 /* Commit of a one-pass step: per layer, flag = OR over the ranks' flags
  * (peer_flags); applied: steps[l] = steps_spec[l] and state_sel[l] flips;
  * rejected: both stay (hiermem/lockfree.py:133-134, 163-164).  applied[]

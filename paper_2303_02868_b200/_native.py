@@ -106,6 +106,9 @@ SIGNATURES = {
                                C.POINTER(AdamHyperC), _OPTS, _P]),
     "hm_dp_onepass_update": (_INT, [_P, _I64, _P, _P, _P, _I64, _P, _P, _INT, _INT, _P, _P, _P, _P,
                                      C.POINTER(AdamHyperC), _OPTS, _P]),
+    "hm_dp_push_grad": (_INT, [_P, _I64, _P, _P, _I64, _P]),
+    "hm_dp_onepass_recv_update": (_INT, [_P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _INT, _INT, _P, _INT, _INT,
+                                          _P, _P, _P, _P, C.POINTER(AdamHyperC), _P]),
     "hm_dp_onepass_finalize": (_INT, [_P, _INT, _INT, _P, _P, _P, _P, _P, _P]),
     "hm_dp_republish_rejected": (_INT, [_P, _I64, _P, _P, _P, _I64, _P, _P, _INT, _INT, _P]),
     "hm_accumulate": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P, _P, _OPTS, _P]),

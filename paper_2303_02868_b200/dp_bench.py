@@ -82,7 +82,10 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
             specs, page, layout, buf, ms = build_state(args, device, world, rank,
                                                        pool_alloc=symmetric_alloc,
                                                        double_buffered=bool(args.dp_onepass))
-            dp = FusedShardedPageStep(buf, ms, mode=args.dp_mode)
+            if args.dp_push < 0:
+                args.dp_push = 0
+            dp = FusedShardedPageStep(buf, ms, mode=args.dp_mode,
+                                      push=bool(args.dp_push) and bool(args.dp_onepass))
             ok = torch.ones(1, device=device)
         except Exception as e:  # e.g. no peer mapping / multicast on this system
             fallback = f"{type(e).__name__}: {e}"[:200]
@@ -234,7 +237,8 @@ def run(args, metric, bytes_per_param, ClockSampler, load_peaks, build_state):
         "run": {"bucket_pages_per_rank": layout.K, "buckets": layout.num_buckets,
                 "sharding": "page-sharded ZeRO-3 (owner = page % N)",
                 "numa_bind": {k: v for k, v in numa.items() if k != "_before"} if numa else None,
-                "dp_mode": (args.dp_mode + (" one-pass" if fused and dp.one_pass else "")) if fallback is None
+                "dp_mode": (args.dp_mode + (" one-pass" if fused and dp.one_pass else "")
+                            + (" push" if fused and getattr(dp, "push", False) else "")) if fallback is None
                            else f"nccl (fallback: {fallback})",
                 "dp_groups": args.dp_groups if pipelined else 1,
                 "dp_reduce_ctas": args.dp_reduce_ctas if pipelined else 0,

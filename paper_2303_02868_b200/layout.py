@@ -152,6 +152,11 @@ class PageLayout:
         reverse=False: src = tensor, dst = pool (pack); True: unpack."""
         return _seg_chunks(self, layer, pool, owned_only, slot, reverse)
 
+    def push_chunks(self) -> np.ndarray:
+        """Units of every page another rank owns, routed to its owner's
+        receive pool (the push form of the one-pass DP step)."""
+        return _push_chunks(self)
+
     def adam_tensor_pos(self, layer: int) -> np.ndarray:
         """uint64 tensor offset of every unit of ``adam_chunks([layer])``
         (owned units, same order): where hm_adam_layer stores the new p32."""
@@ -215,6 +220,30 @@ def _unit_arrays(lay: PageLayout, layer: int, owned_only: bool, bucket: int | No
         out = tuple(np.zeros(0, np.int64) for _ in range(4))
     cache[key] = out
     return out
+
+
+def _push_chunks(lay: PageLayout) -> np.ndarray:
+    """hm_seg_chunk array of every page this rank does NOT own: src_off =
+    16-bit pool offset here, dst_off = state-slot offset on the owner,
+    slot = owner (hm_dp_push_grad)."""
+    cache = lay.__dict__.setdefault("_push_cache", {})
+    if "all" in cache:
+        return cache["all"]
+    parts = []
+    for l in range(len(lay.numels)):
+        for s in lay.segments[l]:
+            if lay.owned(s):
+                continue
+            base16 = lay.slot16(s.page) * lay.E + s.off
+            basest = lay.slot_state(s.page) * lay.E + s.off
+            for d, n in _split(s.off, s.n):
+                parts.append((base16 + d, basest + d, n, lay.owner(s.page)))
+    arr = np.zeros(len(parts), dtype=N.SEG_CHUNK)
+    if parts:
+        a = np.asarray(parts, dtype=np.int64)
+        arr["src_off"], arr["dst_off"], arr["n"], arr["slot"] = a[:, 0], a[:, 1], a[:, 2], a[:, 3]
+    cache["all"] = arr
+    return arr
 
 
 def _adam_chunks(lay: PageLayout, layers: tuple, g_source: str, owned_only: bool,

@@ -242,7 +242,7 @@ class FusedShardedPageStep:
     layers (hm_dp_onepass_update / _finalize / hm_dp_republish_rejected).
     """
 
-    def __init__(self, buffer, masters, group=None, mode: str = "p2p"):
+    def __init__(self, buffer, masters, group=None, mode: str = "p2p", push: bool = False):
         import torch.distributed._symmetric_memory as symm
         lay = buffer.layout
         if masters.layout.numels != lay.numels or masters.layout.world_size != lay.world_size:
@@ -282,6 +282,18 @@ class FusedShardedPageStep:
         self.one_pass = bool(getattr(masters, "_db", False))
         if self.one_pass and mode != "p2p":
             raise ConfigError("the one-pass DP step pulls the gradient with P2P loads (mode='p2p')")
+        # push form of the one-pass step: every rank stores the gradient of the
+        # pages it does not own into the owner's receive pool (N x the owned
+        # 16-bit pages per rank), then the update reads them from local HBM
+        self.push = bool(push)
+        if self.push:
+            if not self.one_pass:
+                raise ConfigError("push=True is a form of the one-pass step (double-buffered MasterState)")
+            self.recv_pool = symm.empty(lay.world_size * lay.elems_state, dtype=buffer._t16, device=self.device)
+            self.h_r = symm.rendezvous(self.recv_pool, gname)
+            self.recv_ptrs = torch.tensor([int(p) for p in self.h_r.buffer_ptrs], dtype=torch.int64,
+                                          device=self.device)
+            self._push_chunks = lay.push_chunks()
 
     @staticmethod
     def _arr(ptrs):
@@ -620,6 +632,25 @@ class FusedShardedPageStep:
                 cache[len(ready)] = [ac[(slots >= grp[0]) & (slots <= grp[-1])].copy()
                                      for grp in layer_groups(lay.numels, len(ready))]
             parts = list(zip(ready, cache[len(ready)]))
+        if self.push:
+            # the push form exchanges the whole gradient before any update:
+            # every group must have landed (one wait per group, then one barrier)
+            for ev, _chunks in parts:
+                if ev is not None:
+                    st.wait_event(ev)
+            with torch.cuda.stream(st):
+                if ready is not None:
+                    self.h_g.barrier(channel=0)
+                D.check(lib.hm_dp_push_grad(D.ptr(eng.desc.static(self._push_chunks)), len(self._push_chunks),
+                                            D.ptr(buf.g16_pool[gsel]), D.ptr(self.recv_ptrs),
+                                            lay.rank * es, D.sptr(st)))
+                self.h_r.barrier(channel=0)                      # every rank's shares landed
+            D.check(lib.hm_dp_onepass_recv_update(
+                D.ptr(eng.desc.static(ac)), len(ac), D.ptr(dgroups), D.ptr(rt), D.ptr(ms._state_sel), es,
+                D.ptr(buf.g16_pool), D.ptr(self.recv_pool), es, lay.rank, self.n, pp, self.n, buf._dt,
+                D.ptr(ms.p32_pool), D.ptr(ms.m32_pool), D.ptr(ms.v32_pool), D.ptr(self.flags_local), hc,
+                D.sptr(st)))
+            parts = []
         for ev, chunks in parts:
             if ev is not None:
                 st.wait_event(ev)

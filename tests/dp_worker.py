@@ -55,7 +55,8 @@ def main():
         ms = LF.MasterState([torch.from_numpy(p) for p in params], page_bytes=PAGE, device=dev, layout=lay,
                             double_buffered=os.environ.get("DP_ONEPASS", "0") == "1")
     onepass = getattr(ms, "_db", False)
-    step = ShardedPageStep(buf, ms) if mode == "nccl" else FusedShardedPageStep(buf, ms, mode=mode)
+    step = ShardedPageStep(buf, ms) if mode == "nccl" else \
+        FusedShardedPageStep(buf, ms, mode=mode, push=os.environ.get("DP_PUSH", "0") == "1")
     from paper_2303_02868_b200 import _native as NL
     NL.check(NL.lib().hm_set_ag_publish(int(os.environ.get("DP_AG_PUBLISH", "0"))))
     NL.check(NL.lib().hm_set_dp_reduce_width(int(os.environ.get("DP_REDUCE_WIDTH", "0"))))

@@ -33,7 +33,9 @@ CASES = [
     (2, "bf16", "p2p", 1, "clip"), (2, "fp16", "nccl", 1, "clip"),   # global grad-norm clip over all ranks
     (2, "bf16", "p2p", 1, "onepass"), (3, "fp16", "p2p", 1, "onepass"),   # ONE fused RS+update+AG kernel
     (2, "bf16", "p2p", 1, "onepass8"),   # ... its 8-peer instantiation
-    (2, "bf16", "p2p", 4, "onepass_ingest")]   # ... group by group while the host gradient arrives
+    (2, "bf16", "p2p", 4, "onepass_ingest"),   # ... group by group while the host gradient arrives
+    (2, "bf16", "p2p", 1, "onepass_push"), (3, "fp16", "p2p", 1, "onepass_push"),   # push form of the exchange
+    (2, "bf16", "p2p", 4, "onepass_push_ingest")]
 SMOKE2 = [CASES[1], CASES[3], CASES[6], CASES[12], CASES[17]]
 
 
@@ -59,9 +61,11 @@ def test_dp_step_two_ranks(bucket, dtype, mode, groups, ctas):
 
 def _run(world, bucket, dtype, mode, groups, ctas):
     agp, upd, ingest, green, width, ld256, host = 0, 0, 0, 0, 0, 0, 0
-    clip, onepass = 0.0, 0
+    clip, onepass, push = 0.0, 0, 0
     if ctas == "clip":
         clip, ctas = 1.0, 0
+    elif ctas in ("onepass_push", "onepass_push_ingest"):
+        onepass, push, ingest, ctas = 1, 1, int(ctas.endswith("ingest")), 0
     elif ctas in ("onepass", "onepass8", "onepass_ingest"):
         onepass, width, ingest = 1, (8 if ctas == "onepass8" else 0), int(ctas == "onepass_ingest")
         ctas = 0
@@ -83,7 +87,7 @@ def _run(world, bucket, dtype, mode, groups, ctas):
                DP_REDUCE_CTAS=str(ctas), DP_AG_PUBLISH=str(agp),
                DP_UPDATE_CTAS=str(upd), DP_INGEST=str(ingest),
                DP_REDUCE_SMS=str(green), DP_REDUCE_WIDTH=str(width), DP_HOST=str(host),
-               DP_CLIP=str(clip), DP_ONEPASS=str(onepass))
+               DP_CLIP=str(clip), DP_ONEPASS=str(onepass), DP_PUSH=str(push))
     visible = os.environ.get("CUDA_VISIBLE_DEVICES")
     ids = visible.split(",") if visible else [str(i) for i in range(torch.cuda.device_count())]
     env["CUDA_VISIBLE_DEVICES"] = ",".join(ids[:world])
