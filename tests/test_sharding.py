@@ -4,7 +4,9 @@
   every bucket holds exactly the pages owner(p) = p % N assigns to r;
 * PageCollectives' in-place bucketed reduce-scatter / all-gather, run with
   world_size 2, 4 and 8 over gloo, hands every owner the sum of its pages and
-  reassembles the pool (the same calls run over NCCL on the GPU box).
+  reassembles the pool (the same calls run over NCCL on the GPU box);
+* the push form's routing table delivers every non-owned element to its
+  owner's receive pool where the owner's update reads it (world 2/4/8).
 """
 import os
 import socket
@@ -124,3 +126,32 @@ def test_modeled_gather_matches_reference_formula():
         assert abs(modeled_gather_s(page, pages, n, bw, lat) - want) < 1e-12
     with pytest.raises(ConfigError):
         modeled_gather_s(page, pages, 0, bw, lat)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_push_routes_every_non_owned_element_to_its_owner(world):
+    """The push form's routing table (layout.push_chunks): simulated with
+    numpy, every rank's non-owned gradient lands in its owner's receive
+    pool at the slot of the sender and the state offset the owner's update
+    reads; together with the owned pages this covers every element once."""
+    lays = [PageLayout(SIZES, PAGE, world_size=world, rank=r, bucket_pages=2) for r in range(world)]
+    es = lays[0].elems_state
+    rng = np.random.default_rng(world)
+    pools = [rng.integers(0, 2 ** 16, lays[0].elems16, dtype=np.uint16) for _ in range(world)]
+    recv = [np.zeros(world * es, np.uint16) for _ in range(world)]
+    for r, lay in enumerate(lays):
+        pc = lay.push_chunks()
+        assert (pc["slot"] != r).all() and (pc["n"] <= 4096).all()
+        for c in pc:
+            dst = r * es + int(c["dst_off"])
+            recv[int(c["slot"])][dst:dst + int(c["n"])] = pools[r][int(c["src_off"]):int(c["src_off"]) + int(c["n"])]
+    covered = 0
+    for r, lay in enumerate(lays):
+        ac = lay.adam_chunks(range(len(SIZES)), "pool", owned_only=True)
+        for c in ac:
+            g, so, n = int(c["g_off"]), int(c["s_off"]), int(c["n"])
+            for q in range(world):
+                share = pools[q][g:g + n] if q == r else recv[r][q * es + so:q * es + so + n]
+                assert np.array_equal(share, pools[q][g:g + n]), (r, q)
+            covered += n
+    assert covered == sum(SIZES)
